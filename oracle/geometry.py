@@ -55,7 +55,7 @@ def _cross_ja(a1, a2, a3):
 
 def _d(arr, axis, D):
     """Collocation derivative of a nodal (n1,n2,n3) array along ``axis``."""
-    return np.moveaxis(np.tensordot(D, arr, axes=([1], [axis])), 0, axis)
+    return np.moveaxis(np.einsum("im,...m->...i", D, np.moveaxis(arr, axis, -1)), -1, axis)
 
 
 def volume_metrics(ctrl, orders, family="LG", form="cross", index=-1):
@@ -75,6 +75,7 @@ def volume_metrics(ctrl, orders, family="LG", form="cross", index=-1):
         av = (a1, a2, a3)
     elif form == "curl":
         X = map_points(ctrl, q[0][0], q[1][0], q[2][0])          # (n1,n2,n3,3)
+        X = X - X.reshape(-1, 3).mean(axis=0)                      # element-local origin
         D = [spectral.differentiation_matrix(int(n), family) for n in orders]
         gX = [[_d(X[..., c], k, D[k]) for k in range(3)] for c in range(3)]  # gX[c][k]
         ja = np.empty((3, 3) + X.shape[:3])

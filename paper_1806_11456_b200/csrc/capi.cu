@@ -1,0 +1,602 @@
+// capi.cu — C-ABI (include/taudg.h) over the sm_100a kernels.
+//
+// Plans own every device allocation they make; fields are caller-owned device
+// buffers.  All launches go to the caller's stream; nothing here synchronises
+// except tdg_plan_create / tdg_transfer_create (uploads).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/taudg.h"
+#include "common.cuh"
+#include "faces.cuh"
+#include "laws.cuh"
+#include "transfer.cuh"
+#include "volume.cuh"
+
+using namespace tdg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      return fail(TDG_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define LAUNCH_CHECK(what)                                                          \
+  do {                                                                              \
+    cudaError_t _e = cudaGetLastError();                                            \
+    if (_e != cudaSuccess)                                                          \
+      return fail(TDG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(_e));   \
+  } while (0)
+
+struct Allocs {
+  std::vector<void*> ptrs;
+  ~Allocs() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+  template <class T>
+  int upload(const T* h, size_t n, T** out) {
+    *out = nullptr;
+    if (n == 0) return TDG_OK;
+    void* d = nullptr;
+    if (cudaMalloc(&d, n * sizeof(T)) != cudaSuccess)
+      return fail(TDG_E_ALLOC, "cudaMalloc failed (" + std::to_string(n * sizeof(T)) + " bytes)");
+    ptrs.push_back(d);
+    if (h && cudaMemcpy(d, h, n * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(TDG_E_CUDA, "cudaMemcpy upload failed");
+    *out = static_cast<T*>(d);
+    return TDG_OK;
+  }
+  template <class T>
+  int zeros(size_t n, T** out) {
+    int rc = upload<T>(nullptr, n, out);
+    if (rc == TDG_OK && n) cudaMemset(*out, 0, n * sizeof(T));
+    return rc;
+  }
+};
+
+int law_nv(int law) { return law == TDG_LAW_NS ? 5 : 1; }
+int law_ngv(int law) { return law == TDG_LAW_NS ? 4 : 1; }
+
+__global__ void k_fill(double* p, double v, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+}  // namespace
+
+struct tdg_plan {
+  DevPlan d{};
+  Allocs mem;
+  int nv = 1, ngv = 1;
+  bool viscous = false;
+  int64_t nodes = 0;
+  std::vector<int> orders_h;      // per slot
+  std::vector<int> elem_id_h;
+  std::vector<long long> node_off_h;
+  size_t smem_lift = 0, smem_flux = 0;
+  int64_t side_nodes = 0;
+};
+
+struct tdg_transfer {
+  DevTransfer d{};
+  Allocs mem;
+  int nwork = 0;
+  size_t smem = 0;
+  int nv = 1;
+};
+
+namespace {
+
+template <class K>
+int allow_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(bytes));
+    if (e != cudaSuccess) return fail(TDG_E_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
+  }
+  return TDG_OK;
+}
+
+template <int LAW>
+int setup_attrs(tdg_plan* p) {
+  using L = Law<LAW>;
+  int rc;
+  if ((rc = allow_smem(k_vol_lift<LAW>, p->smem_lift))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F>, p->smem_flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_A>, p->smem_flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_R>, p->smem_flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_RK>, p->smem_flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU>, p->smem_flux))) return rc;
+  if ((rc = allow_smem(k_face<LAW, false>, face_smem_doubles<LAW, false>() * sizeof(double)))) return rc;
+  if ((rc = allow_smem(k_face<LAW, true>, face_smem_doubles<LAW, true>() * sizeof(double)))) return rc;
+  (void)sizeof(L);
+  return TDG_OK;
+}
+
+// trace -> lift (if viscous) -> face fluxes; leaves fsurf ready for k_vol_flux
+template <int LAW>
+int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
+  using L = Law<LAW>;
+  const DevPlan& d = p->d;
+  if (d.nwork == 0) return TDG_OK;
+  k_trace_q<L::NV><<<d.nwork, ELEM_THREADS, 0, st>>>(d, Q);
+  LAUNCH_CHECK("k_trace_q");
+  auto sides = [&](bool flux) -> int {
+    const int4* items = isolated ? d.side_iso : d.side_bnd;
+    const int n = isolated ? d.nside_iso : d.nside_bnd;
+    if (n > 0) {
+      const int grid = (n + SIDES_PER_BLOCK - 1) / SIDES_PER_BLOCK;
+      if (flux)
+        k_side<LAW, true><<<grid, SIDE_THREADS, 0, st>>>(d, items, n);
+      else
+        k_side<LAW, false><<<grid, SIDE_THREADS, 0, st>>>(d, items, n);
+      LAUNCH_CHECK("k_side");
+    }
+    if (!isolated && d.nfaces > 0) {
+      if (flux)
+        k_face<LAW, true><<<d.nfaces, FACE_THREADS, face_smem_doubles<LAW, true>() * sizeof(double), st>>>(d);
+      else
+        k_face<LAW, false><<<d.nfaces, FACE_THREADS, face_smem_doubles<LAW, false>() * sizeof(double), st>>>(d);
+      LAUNCH_CHECK("k_face");
+    }
+    return TDG_OK;
+  };
+  int rc;
+  if (p->viscous) {
+    if ((rc = sides(false))) return rc;
+    k_vol_lift<LAW><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q);
+    LAUNCH_CHECK("k_vol_lift");
+  }
+  return sides(true);
+}
+
+template <int LAW, int MODE>
+int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cudaStream_t st) {
+  int rc = run_surface<LAW>(p, Q, isolated, st);
+  if (rc) return rc;
+  if (p->d.nwork == 0) return TDG_OK;
+  k_vol_flux<LAW, MODE><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a);
+  LAUNCH_CHECK("k_vol_flux");
+  return TDG_OK;
+}
+
+template <int MODE>
+int dispatch_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cudaStream_t st) {
+  switch (p->d.law) {
+    case TDG_LAW_ADVDIFF: return run_eval<LAW_ADVDIFF, MODE>(p, Q, isolated, a, st);
+    case TDG_LAW_BURGERS: return run_eval<LAW_BURGERS, MODE>(p, Q, isolated, a, st);
+    case TDG_LAW_NS: return run_eval<LAW_NS, MODE>(p, Q, isolated, a, st);
+  }
+  return fail(TDG_E_CONFIG, "unknown law");
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+const char* tdg_last_error(void) { return g_err.c_str(); }
+const char* tdg_version(void) { return "taudg-b200 0.1.0 sm_100a"; }
+
+int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
+  if (!desc || !out) return fail(TDG_E_ARG, "null argument");
+  *out = nullptr;
+  if (desc->law < 0 || desc->law > 2) return fail(TDG_E_CONFIG, "unknown law id");
+  if (desc->tables_len != TABLES_LEN) return fail(TDG_E_CONFIG, "spectral table length mismatch");
+  if (desc->nslots < 0) return fail(TDG_E_ARG, "negative slot count");
+  auto* p = new tdg_plan();
+  p->nv = law_nv(desc->law);
+  p->ngv = law_ngv(desc->law);
+  p->viscous = desc->params[3] > 0.0;
+  const int ns = desc->nslots;
+  p->orders_h.assign(desc->orders, desc->orders + 3 * ns);
+  p->elem_id_h.assign(desc->elem_id, desc->elem_id + ns);
+  p->node_off_h.assign(desc->node_off, desc->node_off + ns + 1);
+  p->nodes = p->node_off_h[ns];
+  for (int s = 0; s < ns; ++s)
+    for (int d = 0; d < 3; ++d) {
+      const int o = p->orders_h[3 * s + d];
+      if (o < 0 || o > 7) {
+        delete p;
+        return fail(TDG_E_CONFIG, "polynomial orders must lie in 0..7 on the device path");
+      }
+      if (desc->family == TDG_LGL && o < 1) {
+        delete p;
+        return fail(TDG_E_CONFIG, "Gauss-Lobatto nodes need orders >= 1");
+      }
+    }
+  DevPlan& d = p->d;
+  d.law = desc->law;
+  d.family = desc->family;
+  std::memcpy(d.prm, desc->params, sizeof(d.prm));
+  d.nslots = ns;
+  d.nfaces = desc->nfaces;
+  d.nbfaces = desc->nbfaces;
+  int rc = TDG_OK;
+  double* tables;
+  int *orders, *elem_id, *affine, *face_info, *bface_info;
+  long long *node_off, *metric_off, *side_off, *face_geo_off, *ghost_off;
+  double *metrics, *sizes, *side_geo, *face_geo, *ghost;
+#define UP(ptr, src, n) if (!rc) rc = p->mem.upload(src, (size_t)(n), &ptr)
+  UP(tables, desc->tables, desc->tables_len);
+  UP(orders, desc->orders, 3 * ns);
+  UP(elem_id, desc->elem_id, ns);
+  UP(node_off, reinterpret_cast<const long long*>(desc->node_off), ns + 1);
+  UP(metric_off, reinterpret_cast<const long long*>(desc->metric_off), ns);
+  UP(affine, desc->affine, ns);
+  UP(metrics, desc->metrics, desc->metrics_len);
+  UP(sizes, desc->sizes, 3 * ns);
+  UP(side_off, reinterpret_cast<const long long*>(desc->side_off), 6 * ns);
+  UP(side_geo, desc->side_geo, 4 * desc->side_nodes);
+  UP(face_info, desc->face_info, 12 * desc->nfaces);
+  UP(face_geo_off, reinterpret_cast<const long long*>(desc->face_geo_off), desc->nfaces);
+  UP(face_geo, desc->face_geo, desc->face_geo_len);
+  UP(bface_info, desc->bface_info, 4 * desc->nbfaces);
+  UP(ghost_off, reinterpret_cast<const long long*>(desc->ghost_off), desc->nbfaces);
+  UP(ghost, desc->ghost, desc->ghost_len);
+#undef UP
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  d.tables = tables;
+  d.orders = orders;
+  d.elem_id = elem_id;
+  d.node_off = node_off;
+  d.metric_off = metric_off;
+  d.affine = affine;
+  d.metrics = metrics;
+  d.sizes = sizes;
+  d.side_off = side_off;
+  d.side_geo = side_geo;
+  d.face_info = face_info;
+  d.face_geo_off = face_geo_off;
+  d.face_geo = face_geo;
+  d.bface_info = bface_info;
+  d.ghost_off = ghost_off;
+  d.ghost = ghost;
+
+  // element work items: runs of identical orders, <= MAXN nodes
+  std::vector<int2> work;
+  for (int s = 0; s < ns;) {
+    const int* o = &p->orders_h[3 * s];
+    const int n = (o[0] + 1) * (o[1] + 1) * (o[2] + 1);
+    const int cap = std::max(1, MAXN / n);
+    int e = s;
+    while (e < ns && e - s < cap && p->orders_h[3 * e] == o[0] && p->orders_h[3 * e + 1] == o[1] &&
+           p->orders_h[3 * e + 2] == o[2])
+      ++e;
+    work.push_back(make_int2(s, e - s));
+    s = e;
+  }
+  std::vector<int4> iso, bnd;
+  iso.reserve(6 * ns);
+  for (int s = 0; s < ns; ++s)
+    for (int side = 0; side < 6; ++side) iso.push_back(make_int4(s, side, -1, -1));
+  for (int f = 0; f < desc->nbfaces; ++f) {
+    const int* b = desc->bface_info + 4 * f;
+    const long long go = desc->ghost_off[f];
+    bnd.push_back(make_int4(b[0], b[1], b[2], static_cast<int>(go)));
+  }
+  int2* work_d;
+  int4 *iso_d, *bnd_d;
+  rc = p->mem.upload(work.data(), work.size(), &work_d);
+  if (!rc) rc = p->mem.upload(iso.data(), iso.size(), &iso_d);
+  if (!rc) rc = p->mem.upload(bnd.data(), bnd.size(), &bnd_d);
+  const size_t sn = static_cast<size_t>(desc->side_nodes);
+  p->side_nodes = desc->side_nodes;
+  const int NG = 3 * p->ngv;
+  double *qtr, *lsurf = nullptr, *gtr = nullptr, *fsurf, *grad = nullptr;
+  if (!rc) rc = p->mem.zeros(sn * p->nv, &qtr);
+  if (!rc) rc = p->mem.zeros(sn * p->nv, &fsurf);
+  if (p->viscous) {
+    if (!rc) rc = p->mem.zeros(sn * NG, &lsurf);
+    if (!rc) rc = p->mem.zeros(sn * NG, &gtr);
+    if (!rc) rc = p->mem.zeros(static_cast<size_t>(p->nodes) * NG, &grad);
+  }
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  d.nwork = static_cast<int>(work.size());
+  d.work = work_d;
+  d.nside_iso = static_cast<int>(iso.size());
+  d.side_iso = iso_d;
+  d.nside_bnd = static_cast<int>(bnd.size());
+  d.side_bnd = bnd_d;
+  d.qtr = qtr;
+  d.lsurf = lsurf;
+  d.gtr = gtr;
+  d.fsurf = fsurf;
+  d.grad = grad;
+  p->smem_lift = static_cast<size_t>(std::max(p->ngv + 9, NG)) * MAXN * sizeof(double);
+  p->smem_flux = static_cast<size_t>(3 * p->nv) * MAXN * sizeof(double);
+  switch (d.law) {
+    case TDG_LAW_ADVDIFF: rc = setup_attrs<LAW_ADVDIFF>(p); break;
+    case TDG_LAW_BURGERS: rc = setup_attrs<LAW_BURGERS>(p); break;
+    default: rc = setup_attrs<LAW_NS>(p); break;
+  }
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  *out = p;
+  return TDG_OK;
+}
+
+int tdg_plan_destroy(tdg_plan* plan) {
+  delete plan;
+  return TDG_OK;
+}
+
+int tdg_plan_size(const tdg_plan* plan, int64_t* nodes, int32_t* nv) {
+  if (!plan) return fail(TDG_E_ARG, "null plan");
+  if (nodes) *nodes = plan->nodes;
+  if (nv) *nv = plan->nv;
+  return TDG_OK;
+}
+
+int tdg_apply(tdg_plan* p, const double* Q, double* F, int isolated, void* stream) {
+  if (!p || !Q || !F) return fail(TDG_E_ARG, "null argument");
+  FluxArgs a{};
+  a.out = F;
+  return dispatch_eval<MODE_F>(p, Q, isolated, a, as_stream(stream));
+}
+
+int tdg_m_inv_apply(tdg_plan* p, const double* Q, const double* add, double* out, int isolated,
+                    void* stream) {
+  if (!p || !Q || !out) return fail(TDG_E_ARG, "null argument");
+  FluxArgs a{};
+  a.out = out;
+  a.X = add;
+  return dispatch_eval<MODE_A>(p, Q, isolated, a, as_stream(stream));
+}
+
+int tdg_residual(tdg_plan* p, const double* Q, const double* S, double* R, double* rnorm,
+                 void* stream) {
+  if (!p || !Q) return fail(TDG_E_ARG, "null argument");
+  cudaStream_t st = as_stream(stream);
+  if (rnorm) CUDA_TRY(cudaMemsetAsync(rnorm, 0, sizeof(double), st));
+  FluxArgs a{};
+  a.S = S;
+  a.out = R;
+  a.norm = rnorm;
+  return dispatch_eval<MODE_R>(p, Q, 0, a, st);
+}
+
+int tdg_tau(tdg_plan* p, const double* Q, const double* S, double* tau, int isolated,
+            void* stream) {
+  if (!p || !Q || !tau) return fail(TDG_E_ARG, "null argument");
+  cudaStream_t st = as_stream(stream);
+  CUDA_TRY(cudaMemsetAsync(tau, 0, sizeof(double) * p->d.nslots, st));
+  FluxArgs a{};
+  a.S = S;
+  a.out = tau;
+  return dispatch_eval<MODE_TAU>(p, Q, isolated, a, st);
+}
+
+int tdg_rk3_stage(tdg_plan* p, double* Q, double* W, const double* S, int stage, const double* dt,
+                  int local, double* rnorm, int32_t* nonfinite, void* stream) {
+  static const double RK_A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};   // timestep.py:18-20
+  static const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+  if (!p || !Q || !W || !dt) return fail(TDG_E_ARG, "null argument");
+  if (stage < 0 || stage > 2) return fail(TDG_E_ARG, "stage must be 0, 1 or 2");
+  FluxArgs a{};
+  a.S = S;
+  a.W = W;
+  a.Qout = Q;
+  a.dt = dt;
+  a.local = local;
+  a.stage = stage;
+  a.rk_a = RK_A[stage];
+  a.rk_b = RK_B[stage];
+  a.norm = rnorm;
+  a.nonfinite = reinterpret_cast<int*>(nonfinite);
+  return dispatch_eval<MODE_RK>(p, Q, 0, a, as_stream(stream));
+}
+
+int tdg_element_dt(tdg_plan* p, const double* Q, double cfl_a, double cfl_v, double* dt_slot,
+                   double* dt_min, void* stream) {
+  if (!p || !Q) return fail(TDG_E_ARG, "null argument");
+  cudaStream_t st = as_stream(stream);
+  if (dt_min) {
+    k_fill<<<1, 32, 0, st>>>(dt_min, HUGE_VAL, 1);
+    LAUNCH_CHECK("k_fill");
+  }
+  if (p->d.nwork == 0) return TDG_OK;
+  switch (p->d.law) {
+    case TDG_LAW_ADVDIFF:
+      k_element_dt<LAW_ADVDIFF><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, Q, cfl_a, cfl_v, dt_slot, dt_min);
+      break;
+    case TDG_LAW_BURGERS:
+      k_element_dt<LAW_BURGERS><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, Q, cfl_a, cfl_v, dt_slot, dt_min);
+      break;
+    default:
+      k_element_dt<LAW_NS><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, Q, cfl_a, cfl_v, dt_slot, dt_min);
+  }
+  LAUNCH_CHECK("k_element_dt");
+  return TDG_OK;
+}
+
+int tdg_norm_inf(tdg_plan* p, const double* X, double* gmax, double* emax, void* stream) {
+  if (!p || !X) return fail(TDG_E_ARG, "null argument");
+  cudaStream_t st = as_stream(stream);
+  if (gmax) CUDA_TRY(cudaMemsetAsync(gmax, 0, sizeof(double), st));
+  if (p->d.nwork == 0) return TDG_OK;
+  if (p->nv == 5)
+    k_norm<5><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, X, gmax, emax, nullptr);
+  else
+    k_norm<1><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, X, gmax, emax, nullptr);
+  LAUNCH_CHECK("k_norm");
+  return TDG_OK;
+}
+
+int tdg_check_finite(tdg_plan* p, const double* X, int32_t* flag, void* stream) {
+  if (!p || !X || !flag) return fail(TDG_E_ARG, "null argument");
+  cudaStream_t st = as_stream(stream);
+  if (p->d.nwork == 0) return TDG_OK;
+  if (p->nv == 5)
+    k_norm<5><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, X, nullptr, nullptr, reinterpret_cast<int*>(flag));
+  else
+    k_norm<1><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, X, nullptr, nullptr, reinterpret_cast<int*>(flag));
+  LAUNCH_CHECK("k_norm");
+  return TDG_OK;
+}
+
+int tdg_copy_gradient(tdg_plan* p, double* dst, void* stream) {
+  if (!p || !dst) return fail(TDG_E_ARG, "null argument");
+  if (!p->viscous) return fail(TDG_E_CONFIG, "inviscid plan has no gradient");
+  CUDA_TRY(cudaMemcpyAsync(dst, p->d.grad, sizeof(double) * p->nodes * 3 * p->ngv,
+                           cudaMemcpyDeviceToDevice, as_stream(stream)));
+  return TDG_OK;
+}
+
+int tdg_debug_copy(tdg_plan* p, int which, double* dst, int64_t* len_out, void* stream) {
+  if (!p) return fail(TDG_E_ARG, "null plan");
+  const int NG = 3 * p->ngv;
+  const double* src = nullptr;
+  int64_t comps = 0;
+  switch (which) {
+    case 0: src = p->d.qtr; comps = p->nv; break;
+    case 1: src = p->d.lsurf; comps = NG; break;
+    case 2: src = p->d.gtr; comps = NG; break;
+    case 3: src = p->d.fsurf; comps = p->nv; break;
+    default: return fail(TDG_E_ARG, "unknown buffer");
+  }
+  const int64_t n = comps * p->side_nodes;
+  if (len_out) *len_out = n;
+  if (!dst) return TDG_OK;
+  if (!src) return fail(TDG_E_CONFIG, "buffer not allocated (inviscid plan)");
+  CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, as_stream(stream)));
+  return TDG_OK;
+}
+
+int tdg_transfer_create(const tdg_transfer_desc* desc, tdg_transfer** out) {
+  if (!desc || !out) return fail(TDG_E_ARG, "null argument");
+  *out = nullptr;
+  if (desc->tables_len != TABLES_LEN) return fail(TDG_E_CONFIG, "spectral table length mismatch");
+  const int ns = desc->nslots;
+  std::vector<int> f_orders(desc->fine_orders, desc->fine_orders + 3 * ns);
+  std::vector<int> c_orders(desc->coarse_orders, desc->coarse_orders + 3 * ns);
+  for (int k = 0; k < 3 * ns; ++k)
+    if (f_orders[k] < 0 || f_orders[k] > 7 || c_orders[k] < 0 || c_orders[k] > 7)
+      return fail(TDG_E_CONFIG, "polynomial orders must lie in 0..7 on the device path");
+  std::unordered_map<int, int> cslot;
+  for (int s = 0; s < ns; ++s) cslot[desc->coarse_elem_id[s]] = s;
+  std::vector<int> c_of_f(ns);
+  for (int s = 0; s < ns; ++s) {
+    auto it = cslot.find(desc->fine_elem_id[s]);
+    if (it == cslot.end()) return fail(TDG_E_CONFIG, "element id missing in coarse field");
+    c_of_f[s] = it->second;
+  }
+  auto* t = new tdg_transfer();
+  t->nv = desc->nv;
+  std::vector<int2> work;
+  for (int s = 0; s < ns;) {
+    const int* fo = &f_orders[3 * s];
+    const int* co = &c_orders[3 * c_of_f[s]];
+    int mx = 1;
+    // largest staging footprint over both transfer directions
+    for (int dir = 0; dir < 2; ++dir) {
+      const int* a = dir ? co : fo;
+      const int* b = dir ? fo : co;
+      const int sizes[4] = {(a[0] + 1) * (a[1] + 1) * (a[2] + 1), (b[0] + 1) * (a[1] + 1) * (a[2] + 1),
+                            (b[0] + 1) * (b[1] + 1) * (a[2] + 1), (b[0] + 1) * (b[1] + 1) * (b[2] + 1)};
+      for (int k = 0; k < 4; ++k) mx = std::max(mx, sizes[k]);
+    }
+    const int cap = std::max(1, MAXN / mx);
+    int e = s;
+    while (e < ns && e - s < cap) {
+      const int* fe = &f_orders[3 * e];
+      const int* ce = &c_orders[3 * c_of_f[e]];
+      if (fe[0] != fo[0] || fe[1] != fo[1] || fe[2] != fo[2] || ce[0] != co[0] || ce[1] != co[1] ||
+          ce[2] != co[2])
+        break;
+      ++e;
+    }
+    work.push_back(make_int2(s, e - s));
+    s = e;
+  }
+  int2* work_d;
+  int *c_d, *fo_d, *co_d;
+  long long *fno_d, *cno_d;
+  double* tab_d;
+  int rc = t->mem.upload(work.data(), work.size(), &work_d);
+  if (!rc) rc = t->mem.upload(c_of_f.data(), c_of_f.size(), &c_d);
+  if (!rc) rc = t->mem.upload(f_orders.data(), f_orders.size(), &fo_d);
+  if (!rc) rc = t->mem.upload(c_orders.data(), c_orders.size(), &co_d);
+  if (!rc) rc = t->mem.upload(reinterpret_cast<const long long*>(desc->fine_node_off), (size_t)ns + 1, &fno_d);
+  if (!rc) rc = t->mem.upload(reinterpret_cast<const long long*>(desc->coarse_node_off), (size_t)ns + 1, &cno_d);
+  if (!rc) rc = t->mem.upload(desc->tables, (size_t)desc->tables_len, &tab_d);
+  if (rc) {
+    delete t;
+    return rc;
+  }
+  t->d.tables = tab_d;
+  t->d.nv = desc->nv;
+  t->d.f_orders = fo_d;
+  t->d.f_node_off = fno_d;
+  t->d.c_orders = co_d;
+  t->d.c_node_off = cno_d;
+  t->d.c_slot_of_f = c_d;
+  t->d.work = work_d;
+  t->nwork = static_cast<int>(work.size());
+  t->smem = 2 * static_cast<size_t>(t->nv) * MAXN * sizeof(double);
+  if ((rc = allow_smem(k_transfer<TR_RESTRICT>, t->smem)) || (rc = allow_smem(k_transfer<TR_PROLONG>, t->smem)) ||
+      (rc = allow_smem(k_transfer<TR_PROLONG_ADD>, t->smem))) {
+    delete t;
+    return rc;
+  }
+  *out = t;
+  return TDG_OK;
+}
+
+int tdg_transfer_destroy(tdg_transfer* t) {
+  delete t;
+  return TDG_OK;
+}
+
+int tdg_restrict(const tdg_transfer* t, const double* fine, double* coarse, void* stream) {
+  if (!t || !fine || !coarse) return fail(TDG_E_ARG, "null argument");
+  if (!t->nwork) return TDG_OK;
+  k_transfer<TR_RESTRICT><<<t->nwork, ELEM_THREADS, t->smem, as_stream(stream)>>>(t->d, fine, nullptr, coarse);
+  LAUNCH_CHECK("k_transfer(restrict)");
+  return TDG_OK;
+}
+
+int tdg_prolong(const tdg_transfer* t, const double* coarse, double* fine, void* stream) {
+  if (!t || !fine || !coarse) return fail(TDG_E_ARG, "null argument");
+  if (!t->nwork) return TDG_OK;
+  k_transfer<TR_PROLONG><<<t->nwork, ELEM_THREADS, t->smem, as_stream(stream)>>>(t->d, coarse, nullptr, fine);
+  LAUNCH_CHECK("k_transfer(prolong)");
+  return TDG_OK;
+}
+
+int tdg_prolong_add(const tdg_transfer* t, const double* Qc, const double* Qc0, double* fine,
+                    void* stream) {
+  if (!t || !fine || !Qc) return fail(TDG_E_ARG, "null argument");
+  if (!t->nwork) return TDG_OK;
+  k_transfer<TR_PROLONG_ADD><<<t->nwork, ELEM_THREADS, t->smem, as_stream(stream)>>>(t->d, Qc, Qc0, fine);
+  LAUNCH_CHECK("k_transfer(prolong_add)");
+  return TDG_OK;
+}
+
+}  // extern "C"

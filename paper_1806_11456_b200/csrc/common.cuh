@@ -1,0 +1,120 @@
+// common.cuh — device-side plan, table layout and reduction helpers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tdg {
+
+// spectral table layout — must match paper_1806_11456_b200/spectral.py
+constexpr int PAD = 8;
+constexpr int OFF_DHAT = 0;
+constexpr int OFF_W = OFF_DHAT + PAD * PAD * PAD;
+constexpr int OFF_BND = OFF_W + PAD * PAD;
+constexpr int OFF_T = OFF_BND + PAD * 2 * PAD;
+constexpr int TABLES_LEN = OFF_T + PAD * PAD * PAD * PAD;
+
+constexpr int ELEM_THREADS = 256;     // element kernels: 8 warps
+constexpr int MAXN = 512;             // nodes per element work item (<= (7+1)^3)
+constexpr int NPT = MAXN / ELEM_THREADS;
+constexpr int FACE_THREADS = 64;      // one interior face (<= 8x8 mortar nodes) per block
+constexpr int SIDE_THREADS = 256;     // four element sides per block
+constexpr int SIDES_PER_BLOCK = SIDE_THREADS / 64;
+
+enum Mode { MODE_F = 0, MODE_A = 1, MODE_R = 2, MODE_RK = 3, MODE_TAU = 4 };
+
+struct DevPlan {
+  int law;
+  int family;
+  double prm[8];
+  const double* tables;
+  int nslots;
+  const int* orders;
+  const int* elem_id;
+  const long long* node_off;
+  const long long* metric_off;
+  const int* affine;
+  const double* metrics;
+  const double* sizes;
+  const long long* side_off;
+  const double* side_geo;
+  int nfaces;
+  const int* face_info;
+  const long long* face_geo_off;
+  const double* face_geo;
+  int nbfaces;
+  const int* bface_info;
+  const long long* ghost_off;
+  const double* ghost;
+  // element work items: (first slot, count), uniform orders inside an item
+  int nwork;
+  const int2* work;
+  // side work items for side kernels: (slot, side | kind<<8), ghost offset
+  int nside_iso;
+  const int4* side_iso;      // isolated: every side of every element
+  int nside_bnd;
+  const int4* side_bnd;      // coupled: boundary faces
+  // scratch (device)
+  double* qtr;    // [side_nodes][nv]      own-order Q traces
+  double* lsurf;  // [side_nodes][3*ngv]   lift surface contributions
+  double* gtr;    // [side_nodes][3*ngv]   gradient traces
+  double* fsurf;  // [side_nodes][nv]      flux surface contributions
+  double* grad;   // [nodes][3*ngv]        lifted gradient
+};
+
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  // IEEE bit patterns of non-negative doubles order like the values (NaN above +inf)
+  atomicMax(reinterpret_cast<unsigned long long*>(addr),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+__device__ __forceinline__ void atomic_min_nonneg(double* addr, double v) {
+  atomicMin(reinterpret_cast<unsigned long long*>(addr),
+            static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// NaN-propagating max (fmax drops NaN)
+__device__ __forceinline__ double nanmax(double a, double b) {
+  return (a != a || b != b) ? __longlong_as_double(0x7ff8000000000000LL) : (a > b ? a : b);
+}
+
+__device__ __forceinline__ double warp_nanmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// block-wide NaN-propagating max of non-negative values -> one atomic per block
+__device__ __forceinline__ void block_max_to(double v, double* out, double* red /*[32]*/) {
+  v = warp_nanmax(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    double x = lane < nw ? red[lane] : 0.0;
+    x = warp_nanmax(x);
+    if (lane == 0 && out) atomic_max_nonneg(out, x);
+  }
+  __syncthreads();
+}
+
+// face coordinates of a side: normal direction and the two tangential ones
+__device__ __forceinline__ void side_dirs(int side, int& d, int& a, int& b) {
+  d = side >> 1;
+  a = (d == 0) ? 1 : 0;
+  b = (d == 2) ? 1 : 2;
+}
+
+}  // namespace tdg

@@ -1,0 +1,303 @@
+// laws.cuh — pointwise physics in registers (FP64).
+//
+// Scalar laws restate /root/reference/pkg/src/taudg/physics.py:49-88 in 3D;
+// Navier-Stokes follows PAPER.md:744-816 with the choices of DESIGN.md
+// (mu = 1 non-dimensional, BR1 on (u, v, w, T), Roe flux without entropy fix,
+// mean-of-sides interface viscous flux).  Parameters (plan prm[8]):
+//   advdiff: a, b, c, mu        burgers: bx, by, bz, mu
+//   NS:      gamma, Pr, M, Re (Re = 0: inviscid)          prm[7] = mu_cfl
+#pragma once
+#include "common.cuh"
+
+namespace tdg {
+
+enum { LAW_ADVDIFF = 0, LAW_BURGERS = 1, LAW_NS = 2 };
+enum { BC_DIRICHLET = 0, BC_FREESTREAM = 1, BC_WALL = 2, BC_SYMMETRY = 3 };
+
+template <int LAW>
+struct Law;
+
+// ---------------------------------------------------------------------------
+template <>
+struct Law<LAW_ADVDIFF> {
+  static constexpr int NV = 1, NGV = 1;
+  __device__ static bool viscous(const double* P) { return P[3] > 0.0; }
+  __device__ static void grad_vars(const double*, const double* q, double* g) { g[0] = q[0]; }
+  __device__ static void adv_flux(const double* P, const double* q, double f[3][NV]) {
+    f[0][0] = P[0] * q[0];
+    f[1][0] = P[1] * q[0];
+    f[2][0] = P[2] * q[0];
+  }
+  // f -= mu grad q   (operators.py:284-287)
+  __device__ static void sub_visc(const double* P, const double*, const double G[3][NGV],
+                                  double f[3][NV]) {
+    f[0][0] -= P[3] * G[0][0];
+    f[1][0] -= P[3] * G[1][0];
+    f[2][0] -= P[3] * G[2][0];
+  }
+  __device__ static void visc_normal(const double* P, const double*, const double G[3][NGV],
+                                     const double* n, double* out) {
+    out[0] = P[3] * (G[0][0] * n[0] + G[1][0] * n[1] + G[2][0] * n[2]);
+  }
+  __device__ static double wave_speed(const double* P, const double*) {
+    return sqrt(P[0] * P[0] + P[1] * P[1] + P[2] * P[2]);
+  }
+  __device__ static void riemann(const double* P, const double* ql, const double* qr,
+                                 const double* n, double* F) {
+    const double an = P[0] * n[0] + P[1] * n[1] + P[2] * n[2];
+    F[0] = 0.5 * an * (ql[0] + qr[0]) + 0.5 * fabs(an) * (ql[0] - qr[0]);
+  }
+  __device__ static void bc_ghost(const double*, const double*, const double*, int,
+                                  const double* ghost, double* qg) { qg[0] = ghost[0]; }
+  __device__ static void bc_lift(const double*, const double*, const double*, int,
+                                 const double* ghost, double* g) { g[0] = ghost[0]; }
+  __device__ static void bc_visc_normal(const double* P, const double* q, const double G[3][NGV],
+                                        const double* n, int, double* out) {
+    visc_normal(P, q, G, n, out);
+  }
+};
+
+// ---------------------------------------------------------------------------
+template <>
+struct Law<LAW_BURGERS> {
+  static constexpr int NV = 1, NGV = 1;
+  __device__ static bool viscous(const double* P) { return P[3] > 0.0; }
+  __device__ static void grad_vars(const double*, const double* q, double* g) { g[0] = q[0]; }
+  __device__ static void adv_flux(const double* P, const double* q, double f[3][NV]) {
+    const double h = 0.5 * q[0] * q[0];
+    f[0][0] = P[0] * h;
+    f[1][0] = P[1] * h;
+    f[2][0] = P[2] * h;
+  }
+  __device__ static void sub_visc(const double* P, const double*, const double G[3][NGV],
+                                  double f[3][NV]) {
+    f[0][0] -= P[3] * G[0][0];
+    f[1][0] -= P[3] * G[1][0];
+    f[2][0] -= P[3] * G[2][0];
+  }
+  __device__ static void visc_normal(const double* P, const double*, const double G[3][NGV],
+                                     const double* n, double* out) {
+    out[0] = P[3] * (G[0][0] * n[0] + G[1][0] * n[1] + G[2][0] * n[2]);
+  }
+  __device__ static double wave_speed(const double* P, const double* q) {
+    return sqrt(P[0] * P[0] + P[1] * P[1] + P[2] * P[2]) * fabs(q[0]);
+  }
+  // Rusanov with lambda = max(|ql|, |qr|)  (physics.py:83-88)
+  __device__ static void riemann(const double* P, const double* ql, const double* qr,
+                                 const double* n, double* F) {
+    const double bn = P[0] * n[0] + P[1] * n[1] + P[2] * n[2];
+    const double lam = fmax(fabs(ql[0]), fabs(qr[0]));
+    F[0] = 0.25 * (ql[0] * ql[0] + qr[0] * qr[0]) * bn - 0.5 * lam * (qr[0] - ql[0]);
+  }
+  __device__ static void bc_ghost(const double*, const double*, const double*, int,
+                                  const double* ghost, double* qg) { qg[0] = ghost[0]; }
+  __device__ static void bc_lift(const double*, const double*, const double*, int,
+                                 const double* ghost, double* g) { g[0] = ghost[0]; }
+  __device__ static void bc_visc_normal(const double* P, const double* q, const double G[3][NGV],
+                                        const double* n, int, double* out) {
+    visc_normal(P, q, G, n, out);
+  }
+};
+
+// ---------------------------------------------------------------------------
+template <>
+struct Law<LAW_NS> {
+  static constexpr int NV = 5, NGV = 4;
+  __device__ static bool viscous(const double* P) { return P[3] > 0.0; }
+
+  __device__ static void prim(const double* P, const double* q, double& rho, double& u,
+                              double& v, double& w, double& p) {
+    rho = q[0];
+    const double ir = 1.0 / rho;
+    u = q[1] * ir;
+    v = q[2] * ir;
+    w = q[3] * ir;
+    p = (P[0] - 1.0) * (q[4] - 0.5 * rho * (u * u + v * v + w * w));
+  }
+  __device__ static void grad_vars(const double* P, const double* q, double* g) {
+    double rho, u, v, w, p;
+    prim(P, q, rho, u, v, w, p);
+    g[0] = u;
+    g[1] = v;
+    g[2] = w;
+    g[3] = P[0] * P[2] * P[2] * p / rho;
+  }
+  __device__ static void adv_flux(const double* P, const double* q, double f[3][NV]) {
+    double rho, u, v, w, p;
+    prim(P, q, rho, u, v, w, p);
+    const double H = q[4] + p;
+    const double vel[3] = {u, v, w};
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double vd = vel[d];
+      f[d][0] = q[0] * vd;
+      f[d][1] = q[1] * vd;
+      f[d][2] = q[2] * vd;
+      f[d][3] = q[3] * vd;
+      f[d][1 + d] += p;
+      f[d][4] = vd * H;
+    }
+  }
+  // viscous flux (1/Re)[0, tau_d., u.tau_d + kappa T_d] in direction d
+  __device__ static void visc_dir(const double* P, double u, double v, double w,
+                                  const double G[3][NGV], int d, double* fv) {
+    const double inv_re = 1.0 / P[3];
+    const double kappa = 1.0 / ((P[0] - 1.0) * P[1] * P[2] * P[2]);
+    const double div = G[0][0] + G[1][1] + G[2][2];
+    double tau[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double t = G[d][i] + G[i][d];
+      if (i == d) t -= (2.0 / 3.0) * div;
+      tau[i] = t;
+    }
+    fv[0] = 0.0;
+    fv[1] = inv_re * tau[0];
+    fv[2] = inv_re * tau[1];
+    fv[3] = inv_re * tau[2];
+    fv[4] = inv_re * (u * tau[0] + v * tau[1] + w * tau[2] + kappa * G[d][3]);
+  }
+  __device__ static void sub_visc(const double* P, const double* q, const double G[3][NGV],
+                                  double f[3][NV]) {
+    double rho, u, v, w, p;
+    prim(P, q, rho, u, v, w, p);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double fv[5];
+      visc_dir(P, u, v, w, G, d, fv);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) f[d][k] -= fv[k];
+    }
+  }
+  __device__ static void visc_normal(const double* P, const double* q, const double G[3][NGV],
+                                     const double* n, double* out) {
+    double rho, u, v, w, p;
+    prim(P, q, rho, u, v, w, p);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) out[k] = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double fv[5];
+      visc_dir(P, u, v, w, G, d, fv);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) out[k] += n[d] * fv[k];
+    }
+  }
+  __device__ static double wave_speed(const double* P, const double* q) {
+    double rho, u, v, w, p;
+    prim(P, q, rho, u, v, w, p);
+    return sqrt(u * u + v * v + w * w) + sqrt(P[0] * p / rho);
+  }
+  // Roe flux, no entropy fix (oracle/physics.py NavierStokes.riemann)
+  __device__ static void riemann(const double* P, const double* ql, const double* qr,
+                                 const double* n, double* F) {
+    const double g = P[0];
+    double rl, ul, vl, wl, pl, rr, ur, vr, wr, pr;
+    prim(P, ql, rl, ul, vl, wl, pl);
+    prim(P, qr, rr, ur, vr, wr, pr);
+    const double nx = n[0], ny = n[1], nz = n[2];
+    const double vnl = ul * nx + vl * ny + wl * nz;
+    const double vnr = ur * nx + vr * ny + wr * nz;
+    const double Hl = (ql[4] + pl) / rl;
+    const double Hr = (qr[4] + pr) / rr;
+    const double sl = sqrt(rl), sr = sqrt(rr);
+    const double inv = 1.0 / (sl + sr);
+    const double ut = (sl * ul + sr * ur) * inv;
+    const double vt = (sl * vl + sr * vr) * inv;
+    const double wt = (sl * wl + sr * wr) * inv;
+    const double Ht = (sl * Hl + sr * Hr) * inv;
+    const double rt = sl * sr;
+    const double q2 = ut * ut + vt * vt + wt * wt;
+    const double c2 = (g - 1.0) * (Ht - 0.5 * q2);
+    const double ct = sqrt(c2);
+    const double vnt = ut * nx + vt * ny + wt * nz;
+    const double drho = rr - rl, dp = pr - pl;
+    const double du = ur - ul, dv = vr - vl, dw = wr - wl;
+    const double dvn = vnr - vnl;
+    const double a1 = (dp - rt * ct * dvn) / (2.0 * c2);
+    const double a2 = drho - dp / c2;
+    const double a5 = (dp + rt * ct * dvn) / (2.0 * c2);
+    const double l1 = fabs(vnt - ct), l2 = fabs(vnt), l5 = fabs(vnt + ct);
+    const double sx = du - dvn * nx, sy = dv - dvn * ny, sz = dw - dvn * nz;
+    double D[5];
+    D[0] = l1 * a1 + l2 * a2 + l5 * a5;
+    D[1] = l1 * a1 * (ut - ct * nx) + l2 * (a2 * ut + rt * sx) + l5 * a5 * (ut + ct * nx);
+    D[2] = l1 * a1 * (vt - ct * ny) + l2 * (a2 * vt + rt * sy) + l5 * a5 * (vt + ct * ny);
+    D[3] = l1 * a1 * (wt - ct * nz) + l2 * (a2 * wt + rt * sz) + l5 * a5 * (wt + ct * nz);
+    D[4] = l1 * a1 * (Ht - ct * vnt) +
+           l2 * (a2 * 0.5 * q2 + rt * (ut * du + vt * dv + wt * dw - vnt * dvn)) +
+           l5 * a5 * (Ht + ct * vnt);
+    // 0.5 (Fn(ql) + Fn(qr))
+    const double Hql = ql[4] + pl, Hqr = qr[4] + pr;
+    F[0] = 0.5 * (ql[0] * vnl + qr[0] * vnr) - 0.5 * D[0];
+    F[1] = 0.5 * (ql[1] * vnl + pl * nx + qr[1] * vnr + pr * nx) - 0.5 * D[1];
+    F[2] = 0.5 * (ql[2] * vnl + pl * ny + qr[2] * vnr + pr * ny) - 0.5 * D[2];
+    F[3] = 0.5 * (ql[3] * vnl + pl * nz + qr[3] * vnr + pr * nz) - 0.5 * D[3];
+    F[4] = 0.5 * (vnl * Hql + vnr * Hqr) - 0.5 * D[4];
+  }
+  // boundary states (oracle/physics.py NavierStokes.bc_*)
+  __device__ static void bc_ghost(const double*, const double* q, const double* n, int kind,
+                                  const double* ghost, double* qg) {
+    if (kind == BC_WALL) {
+      qg[0] = q[0];
+      qg[1] = -q[1];
+      qg[2] = -q[2];
+      qg[3] = -q[3];
+      qg[4] = q[4];
+    } else if (kind == BC_SYMMETRY) {
+      const double mn = q[1] * n[0] + q[2] * n[1] + q[3] * n[2];
+      qg[0] = q[0];
+      qg[1] = q[1] - 2.0 * mn * n[0];
+      qg[2] = q[2] - 2.0 * mn * n[1];
+      qg[3] = q[3] - 2.0 * mn * n[2];
+      qg[4] = q[4];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) qg[k] = ghost[k];
+    }
+  }
+  __device__ static void bc_lift(const double* P, const double* q, const double* n, int kind,
+                                 const double* ghost, double* g) {
+    if (kind == BC_WALL) {
+      grad_vars(P, q, g);
+      g[0] = g[1] = g[2] = 0.0;
+    } else if (kind == BC_SYMMETRY) {
+      grad_vars(P, q, g);
+      const double vn = g[0] * n[0] + g[1] * n[1] + g[2] * n[2];
+      g[0] -= vn * n[0];
+      g[1] -= vn * n[1];
+      g[2] -= vn * n[2];
+    } else {
+      grad_vars(P, ghost, g);
+    }
+  }
+  __device__ static void bc_visc_normal(const double* P, const double* q, const double G[3][NGV],
+                                        const double* n, int kind, double* out) {
+    if (kind == BC_SYMMETRY) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) out[k] = 0.0;
+    } else if (kind == BC_WALL) {
+      double Gw[3][NGV];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        Gw[d][0] = G[d][0];
+        Gw[d][1] = G[d][1];
+        Gw[d][2] = G[d][2];
+        Gw[d][3] = 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 5; ++k) out[k] = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        double fv[5];
+        visc_dir(P, 0.0, 0.0, 0.0, Gw, d, fv);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) out[k] += n[d] * fv[k];
+      }
+    } else {
+      visc_normal(P, q, G, n, out);
+    }
+  }
+};
+
+}  // namespace tdg

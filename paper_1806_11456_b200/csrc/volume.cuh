@@ -1,0 +1,501 @@
+// volume.cuh — element-parallel kernels over shape-uniform work items.
+//
+// A work item is a run of slots of ONE bucket (same (N1,N2,N3)), at most MAXN
+// nodes in total; a 256-thread block owns one item, each thread up to NPT
+// nodes.  Spectral tables of the bucket's three orders are staged in shared
+// memory; contravariant fluxes are staged in shared memory and contracted
+// direction by direction with the weighted derivative matrices (the weak
+// divergence of operators.py:196-200).
+#pragma once
+#include "common.cuh"
+#include "laws.cuh"
+
+namespace tdg {
+
+struct ElemTables {
+  double dh[3][64];   // Dhat[m*8+i] per direction
+  double w[3][8];
+  double bnd[3][16];  // l_i(-1) at [i], l_i(+1) at [8+i]
+  double red[32];
+  unsigned long long emax[64];  // per-element max bits (tau / dt)
+};
+
+__device__ __forceinline__ void load_tables(const DevPlan& P, int N1, int N2, int N3,
+                                            ElemTables& T) {
+  const int No[3] = {N1, N2, N3};
+  for (int u = threadIdx.x; u < 3 * 64; u += blockDim.x) {
+    const int d = u / 64, k = u % 64;
+    T.dh[d][k] = P.tables[OFF_DHAT + No[d] * 64 + k];
+  }
+  for (int u = threadIdx.x; u < 3 * 8; u += blockDim.x) {
+    const int d = u / 8, k = u % 8;
+    T.w[d][k] = P.tables[OFF_W + No[d] * 8 + k];
+  }
+  for (int u = threadIdx.x; u < 3 * 16; u += blockDim.x) {
+    const int d = u / 16, k = u % 16;
+    T.bnd[d][k] = P.tables[OFF_BND + No[d] * 16 + k];
+  }
+  for (int u = threadIdx.x; u < 64; u += blockDim.x) T.emax[u] = 0ull;
+}
+
+__device__ __forceinline__ const double* metric_ptr(const DevPlan& P, int slot, int node, int n,
+                                                    int& stride) {
+  const bool aff = P.affine[slot] != 0;
+  stride = aff ? 1 : n;
+  return P.metrics + P.metric_off[slot] + (aff ? 0 : node);
+}
+
+// ---------------------------------------------------------------------------
+// Q traces on the six sides at own order (operators.py:73-80, 185-194)
+template <int NV>
+__global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const double* __restrict__ Q) {
+  __shared__ double sb[3][16];
+  const int2 wi = P.work[blockIdx.x];
+  const int* od = P.orders + 3 * wi.x;
+  const int No[3] = {od[0], od[1], od[2]};
+  for (int u = threadIdx.x; u < 48; u += blockDim.x)
+    sb[u / 16][u % 16] = P.tables[OFF_BND + No[u / 16] * 16 + (u % 16)];
+  __syncthreads();
+  const int np[3] = {No[0] + 1, No[1] + 1, No[2] + 1};
+  const int n = np[0] * np[1] * np[2];
+  const int strides[3] = {1, np[0], np[0] * np[1]};
+  const int items = wi.y * 6 * 64;
+  const bool lgl = P.family == 1;
+  for (int u = threadIdx.x; u < items; u += blockDim.x) {
+    const int e = u / 384, s = (u / 64) % 6, kf = u % 64;
+    int d, a, b;
+    side_dirs(s, d, a, b);
+    const int nf = np[a] * np[b];
+    if (kf >= nf) continue;
+    const int ia = kf % np[a], ib = kf / np[a];
+    const int slot = wi.x + e;
+    const long long base = P.node_off[slot] * NV;
+    const long long so = P.side_off[slot * 6 + s];
+    const int off0 = ia * strides[a] + ib * strides[b];
+    const double* row = &sb[d][(s & 1) * 8];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const double* qv = Q + base + (long long)v * n + off0;
+      double acc;
+      if (lgl) {
+        acc = qv[(s & 1) ? (np[d] - 1) * strides[d] : 0];
+      } else {
+        acc = 0.0;
+        for (int m = 0; m < np[d]; ++m) acc += row[m] * qv[m * strides[d]];
+      }
+      P.qtr[so * NV + (long long)v * nf + kf] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// BR1 lift, volume part + scatter of the face contributions, times M^-1
+// (operators.py:224-265); writes the gradient and its side traces.
+template <int LAW>
+__global__ void __launch_bounds__(ELEM_THREADS) k_vol_lift(DevPlan P, const double* __restrict__ Q) {
+  using L = Law<LAW>;
+  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
+  __shared__ ElemTables T;
+  extern __shared__ double sm[];
+  const int2 wi = P.work[blockIdx.x];
+  const int* od = P.orders + 3 * wi.x;
+  const int N1 = od[0], N2 = od[1], N3 = od[2];
+  load_tables(P, N1, N2, N3, T);
+  const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
+  const int n = n1p * n2p * n3p, tot = wi.y * n;
+  double* gs = sm;               // [NGV][tot]
+  double* js = sm + NGV * tot;   // [9][tot]
+  __syncthreads();
+
+#pragma unroll
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * ELEM_THREADS;
+    if (t < tot) {
+      const int e = t / n, node = t - e * n, slot = wi.x + e;
+      const long long base = P.node_off[slot] * NV;
+      double q[NV], g[NGV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) q[v] = Q[base + (long long)v * n + node];
+      L::grad_vars(P.prm, q, g);
+#pragma unroll
+      for (int k = 0; k < NGV; ++k) gs[k * tot + t] = g[k];
+      int ms;
+      const double* m = metric_ptr(P, slot, node, n, ms);
+#pragma unroll
+      for (int c = 0; c < 9; ++c) js[c * tot + t] = m[(1 + c) * ms];
+    }
+  }
+  __syncthreads();
+
+  double Greg[NPT][NG];
+#pragma unroll
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * ELEM_THREADS;
+    if (t < tot) {
+      const int e = t / n, node = t - e * n, slot = wi.x + e;
+      const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+      const int eb = e * n;
+      double acc[NG];
+#pragma unroll
+      for (int c = 0; c < NG; ++c) acc[c] = 0.0;
+      // xi direction
+      {
+        const double wo = T.w[1][j] * T.w[2][k];
+        for (int m = 0; m < n1p; ++m) {
+          const int idx = eb + m + n1p * (j + n2p * k);
+          const double dw = T.dh[0][m * 8 + i] * wo;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const double ja = js[(0 * 3 + d) * tot + idx] * dw;
+#pragma unroll
+            for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+          }
+        }
+      }
+      {
+        const double wo = T.w[0][i] * T.w[2][k];
+        for (int m = 0; m < n2p; ++m) {
+          const int idx = eb + i + n1p * (m + n2p * k);
+          const double dw = T.dh[1][m * 8 + j] * wo;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const double ja = js[(1 * 3 + d) * tot + idx] * dw;
+#pragma unroll
+            for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+          }
+        }
+      }
+      {
+        const double wo = T.w[0][i] * T.w[1][j];
+        for (int m = 0; m < n3p; ++m) {
+          const int idx = eb + i + n1p * (j + n2p * m);
+          const double dw = T.dh[2][m * 8 + k] * wo;
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const double ja = js[(2 * 3 + d) * tot + idx] * dw;
+#pragma unroll
+            for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+          }
+        }
+      }
+      // surface scatter of the lift contributions
+      const int ijk[3] = {i, j, k};
+      const int np[3] = {n1p, n2p, n3p};
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        int d, a, b;
+        side_dirs(s, d, a, b);
+        const double l = T.bnd[d][(s & 1) * 8 + ijk[d]];
+        if (l == 0.0) continue;
+        const int nf = np[a] * np[b];
+        const int kf = ijk[a] + np[a] * ijk[b];
+        const double lw = l * T.w[a][ijk[a]] * T.w[b][ijk[b]];
+        const double* src = P.lsurf + P.side_off[slot * 6 + s] * NG + kf;
+#pragma unroll
+        for (int c = 0; c < NG; ++c) acc[c] += lw * src[(long long)c * nf];
+      }
+      int ms;
+      const double* mp = metric_ptr(P, slot, node, n, ms);
+      const double invm = 1.0 / (T.w[0][i] * T.w[1][j] * T.w[2][k] * mp[0]);
+#pragma unroll
+      for (int c = 0; c < NG; ++c) Greg[r][c] = acc[c] * invm;
+    }
+  }
+  __syncthreads();
+  // stage G in shared memory (reusing gs/js) and write it out
+  double* G = sm;   // [NG][tot]
+#pragma unroll
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * ELEM_THREADS;
+    if (t < tot) {
+      const int e = t / n, node = t - e * n, slot = wi.x + e;
+      const long long gb = P.node_off[slot] * NG;
+#pragma unroll
+      for (int c = 0; c < NG; ++c) {
+        G[c * tot + t] = Greg[r][c];
+        P.grad[gb + (long long)c * n + node] = Greg[r][c];
+      }
+    }
+  }
+  __syncthreads();
+  // gradient traces on the six sides
+  const int np[3] = {n1p, n2p, n3p};
+  const int strides[3] = {1, n1p, n1p * n2p};
+  const int items = wi.y * 6 * 64;
+  for (int u = threadIdx.x; u < items; u += blockDim.x) {
+    const int e = u / 384, s = (u / 64) % 6, kf = u % 64;
+    int d, a, b;
+    side_dirs(s, d, a, b);
+    const int nf = np[a] * np[b];
+    if (kf >= nf) continue;
+    const int ia = kf % np[a], ib = kf / np[a];
+    const int slot = wi.x + e;
+    const long long so = P.side_off[slot * 6 + s];
+    const int off0 = e * n + ia * strides[a] + ib * strides[b];
+    const double* row = &T.bnd[d][(s & 1) * 8];
+    for (int c = 0; c < NG; ++c) {
+      double acc = 0.0;
+      for (int m = 0; m < np[d]; ++m) acc += row[m] * G[c * tot + off0 + m * strides[d]];
+      P.gtr[so * NG + (long long)c * nf + kf] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Flux divergence + surface scatter + epilogue (operators.py:283-290, 337-364;
+// timestep.py:100-112 for MODE_RK).
+struct FluxArgs {
+  const double* S;     // source (nullable)
+  const double* X;     // additive term for MODE_A (nullable)
+  double* out;         // output field (MODE_F/A/R) or tau by element id (MODE_TAU)
+  double* W;           // RK register
+  double* Qout;        // RK: updated state (== Q)
+  const double* dt;
+  int local;
+  int stage;
+  double rk_a, rk_b;
+  double* norm;        // max |r|
+  int* nonfinite;
+};
+
+template <int LAW, int MODE>
+__global__ void __launch_bounds__(ELEM_THREADS) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
+  using L = Law<LAW>;
+  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
+  __shared__ ElemTables T;
+  extern __shared__ double sm[];
+  const int2 wi = P.work[blockIdx.x];
+  const int* od = P.orders + 3 * wi.x;
+  const int N1 = od[0], N2 = od[1], N3 = od[2];
+  load_tables(P, N1, N2, N3, T);
+  const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
+  const int n = n1p * n2p * n3p, tot = wi.y * n;
+  const bool visc = L::viscous(P.prm);
+  double* ft = sm;   // [3][NV][tot]
+  __syncthreads();
+
+#pragma unroll
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * ELEM_THREADS;
+    if (t < tot) {
+      const int e = t / n, node = t - e * n, slot = wi.x + e;
+      const long long base = P.node_off[slot] * NV;
+      double q[NV], f[3][NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) q[v] = Q[base + (long long)v * n + node];
+      L::adv_flux(P.prm, q, f);
+      if (visc) {
+        double G[3][NGV];
+        const double* gp = P.grad + P.node_off[slot] * NG + node;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int k = 0; k < NGV; ++k) G[d][k] = gp[(long long)(d * NGV + k) * n];
+        L::sub_visc(P.prm, q, G, f);
+      }
+      int ms;
+      const double* m = metric_ptr(P, slot, node, n, ms);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double j0 = m[(1 + 3 * i) * ms], j1 = m[(2 + 3 * i) * ms], j2 = m[(3 + 3 * i) * ms];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          ft[(i * NV + v) * tot + t] = j0 * f[0][v] + j1 * f[1][v] + j2 * f[2][v];
+      }
+    }
+  }
+  __syncthreads();
+
+  double rmax = 0.0;
+#pragma unroll
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * ELEM_THREADS;
+    if (t < tot) {
+      const int e = t / n, node = t - e * n, slot = wi.x + e;
+      const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+      const int eb = e * n;
+      double F[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) F[v] = 0.0;
+      {
+        const double wo = T.w[1][j] * T.w[2][k];
+        for (int m = 0; m < n1p; ++m) {
+          const int idx = eb + m + n1p * (j + n2p * k);
+          const double dw = T.dh[0][m * 8 + i] * wo;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) F[v] -= dw * ft[(0 * NV + v) * tot + idx];
+        }
+      }
+      {
+        const double wo = T.w[0][i] * T.w[2][k];
+        for (int m = 0; m < n2p; ++m) {
+          const int idx = eb + i + n1p * (m + n2p * k);
+          const double dw = T.dh[1][m * 8 + j] * wo;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) F[v] -= dw * ft[(1 * NV + v) * tot + idx];
+        }
+      }
+      {
+        const double wo = T.w[0][i] * T.w[1][j];
+        for (int m = 0; m < n3p; ++m) {
+          const int idx = eb + i + n1p * (j + n2p * m);
+          const double dw = T.dh[2][m * 8 + k] * wo;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) F[v] -= dw * ft[(2 * NV + v) * tot + idx];
+        }
+      }
+      const int ijk[3] = {i, j, k};
+      const int np[3] = {n1p, n2p, n3p};
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        int d, a, b;
+        side_dirs(s, d, a, b);
+        const double l = T.bnd[d][(s & 1) * 8 + ijk[d]];
+        if (l == 0.0) continue;
+        const int nf = np[a] * np[b];
+        const int kf = ijk[a] + np[a] * ijk[b];
+        const double lw = l * T.w[a][ijk[a]] * T.w[b][ijk[b]];
+        const double* src = P.fsurf + P.side_off[slot * 6 + s] * NV + kf;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) F[v] += lw * src[(long long)v * nf];
+      }
+      const long long base = P.node_off[slot] * NV + node;
+      int ms;
+      const double* mp = metric_ptr(P, slot, node, n, ms);
+      const double mass = T.w[0][i] * T.w[1][j] * T.w[2][k] * mp[0];
+      const double invm = 1.0 / mass;
+      if (MODE == MODE_F) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) A.out[base + (long long)v * n] = F[v];
+      } else if (MODE == MODE_A) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double a = F[v] * invm;
+          if (A.X) a += A.X[base + (long long)v * n];
+          A.out[base + (long long)v * n] = a;
+        }
+      } else if (MODE == MODE_R) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double s = A.S ? A.S[base + (long long)v * n] : 0.0;
+          const double rv = s - F[v] * invm;
+          if (A.out) A.out[base + (long long)v * n] = rv;
+          rmax = nanmax(rmax, fabs(rv));
+        }
+      } else if (MODE == MODE_RK) {
+        const double dtv = A.local ? A.dt[slot] : A.dt[0];
+        bool bad = false;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const long long ix = base + (long long)v * n;
+          const double s = A.S ? A.S[ix] : 0.0;
+          const double rv = s - F[v] * invm;
+          rmax = nanmax(rmax, fabs(rv));
+          const double wv = (A.stage == 0) ? rv : A.rk_a * A.W[ix] + rv;
+          A.W[ix] = wv;
+          const double qn = A.Qout[ix] + A.rk_b * dtv * wv;
+          A.Qout[ix] = qn;
+          bad |= !isfinite(qn);
+        }
+        if (bad && A.nonfinite) *A.nonfinite = 1;
+      } else if (MODE == MODE_TAU) {
+        double tv = 0.0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double s = A.S ? A.S[base + (long long)v * n] : 0.0;
+          tv = nanmax(tv, fabs(mass * s - F[v]));
+        }
+        atomicMax(&T.emax[e], static_cast<unsigned long long>(__double_as_longlong(tv)));
+      }
+    }
+  }
+  if (MODE == MODE_R || (MODE == MODE_RK)) {
+    if (A.norm && (MODE == MODE_R || A.stage == 0)) block_max_to(rmax, A.norm, T.red);
+  }
+  if (MODE == MODE_TAU) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < wi.y; e += blockDim.x)
+      atomic_max_nonneg(A.out + P.elem_id[wi.x + e], __longlong_as_double((long long)T.emax[e]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-element pseudo-time step (timestep.py:40-66)
+template <int LAW>
+__global__ void __launch_bounds__(ELEM_THREADS) k_element_dt(DevPlan P, const double* __restrict__ Q,
+                                                             double cfl_a, double cfl_v,
+                                                             double* dt_slot, double* dt_min) {
+  using L = Law<LAW>;
+  constexpr int NV = L::NV;
+  __shared__ unsigned long long smax[64];
+  const int2 wi = P.work[blockIdx.x];
+  const int* od = P.orders + 3 * wi.x;
+  const int No[3] = {od[0], od[1], od[2]};
+  const int n = (No[0] + 1) * (No[1] + 1) * (No[2] + 1), tot = wi.y * n;
+  for (int u = threadIdx.x; u < 64; u += blockDim.x) smax[u] = 0ull;
+  __syncthreads();
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int e = t / n, node = t - e * n, slot = wi.x + e;
+    const long long base = P.node_off[slot] * NV;
+    double q[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) q[v] = Q[base + (long long)v * n + node];
+    const double s = L::wave_speed(P.prm, q);
+    atomicMax(&smax[e], static_cast<unsigned long long>(__double_as_longlong(nanmax(s, 0.0))));
+  }
+  __syncthreads();
+  const double mu = P.prm[7];
+  for (int e = threadIdx.x; e < wi.y; e += blockDim.x) {
+    const int slot = wi.x + e;
+    const double sm = __longlong_as_double((long long)smax[e]);
+    double dt = __longlong_as_double(0x7ff0000000000000LL);
+    for (int d = 0; d < 3; ++d) {
+      if (No[d] == 0) continue;
+      const double nn = (double)(No[d] > 1 ? No[d] : 1);
+      const double h = P.sizes[slot * 3 + d];
+      if (sm > 0.0) dt = fmin(dt, cfl_a * h / (sm * nn * nn));
+      if (mu > 0.0) dt = fmin(dt, cfl_v * h * h / (mu * nn * nn * nn * nn));
+    }
+    if (sm != sm) dt = sm;   // NaN state propagates
+    if (dt_slot) dt_slot[slot] = dt;
+    if (dt_min) atomic_min_nonneg(dt_min, dt);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// max |X| over everything and per element; non-finite flag (fields.py:144-162)
+template <int NV>
+__global__ void __launch_bounds__(ELEM_THREADS) k_norm(DevPlan P, const double* __restrict__ X,
+                                                       double* gmax, double* emax_out, int* flag) {
+  __shared__ unsigned long long emax[64];
+  __shared__ double red[32];
+  const int2 wi = P.work[blockIdx.x];
+  const int* od = P.orders + 3 * wi.x;
+  const int n = (od[0] + 1) * (od[1] + 1) * (od[2] + 1), tot = wi.y * n;
+  for (int u = threadIdx.x; u < 64; u += blockDim.x) emax[u] = 0ull;
+  __syncthreads();
+  double m = 0.0;
+  bool bad = false;
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int e = t / n, node = t - e * n, slot = wi.x + e;
+    const long long base = P.node_off[slot] * NV + node;
+    double em = 0.0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const double x = X[base + (long long)v * n];
+      em = nanmax(em, fabs(x));
+      bad |= !isfinite(x);
+    }
+    m = nanmax(m, em);
+    if (emax_out) atomicMax(&emax[e], static_cast<unsigned long long>(__double_as_longlong(em)));
+  }
+  if (bad && flag) *flag = 1;
+  if (gmax) block_max_to(m, gmax, red);
+  if (emax_out) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < wi.y; e += blockDim.x)
+      emax_out[P.elem_id[wi.x + e]] = __longlong_as_double((long long)emax[e]);
+  }
+}
+
+}  // namespace tdg

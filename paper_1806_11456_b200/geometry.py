@@ -1,0 +1,141 @@
+"""Element metrics and face geometry, vectorised over a bucket (host setup).
+
+3D counterpart of /root/reference/pkg/src/taudg/mesh.py:103-192.  Two metric
+forms:
+
+* "cross": Ja^i = a_j x a_k from the analytic mapping derivatives, pointwise
+  (the reference's cross-product form, mesh.py:155-160); face and mortar
+  sigma/normal are evaluated analytically at their points (mesh.py:167-187).
+* "curl":  the invariant curl form by collocation at the
+  solution nodes; face values are the trace of that volume polynomial, mortar
+  values its interpolation (free-stream preserving on conforming 3D meshes).
+
+All arrays carry a leading bucket axis B.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import spectral
+from .errors import MeshError
+
+
+def _ctrl(m):
+    return np.linspace(-1.0, 1.0, m + 1)
+
+
+def _lag(m, pts):
+    return spectral.lagrange_matrix(_ctrl(m), pts)
+
+
+def _dlag(m, pts):
+    return spectral.lagrange_matrix(_ctrl(m), pts) @ spectral.derivative_matrix(_ctrl(m))
+
+
+def map_points(nodes, xs, ys, zs):
+    """nodes (B, a1, a2, a3, 3) -> (B, len xs, len ys, len zs, 3)."""
+    m = [s - 1 for s in nodes.shape[1:4]]
+    return np.einsum("ia,jb,kc,Eabcx->Eijkx", _lag(m[0], xs), _lag(m[1], ys), _lag(m[2], zs), nodes)
+
+
+def map_derivs(nodes, xs, ys, zs):
+    m = [s - 1 for s in nodes.shape[1:4]]
+    L = [_lag(m[0], xs), _lag(m[1], ys), _lag(m[2], zs)]
+    dL = [_dlag(m[0], xs), _dlag(m[1], ys), _dlag(m[2], zs)]
+    out = []
+    for d in range(3):
+        M = [dL[k] if k == d else L[k] for k in range(3)]
+        out.append(np.einsum("ia,jb,kc,Eabcx->Eijkx", M[0], M[1], M[2], nodes))
+    return out
+
+
+def _coll(arr, axis, D):
+    """Collocation derivative along spatial ``axis`` (1..3) of (B, n1, n2, n3)."""
+    return np.moveaxis(np.einsum("im,...m->...i", D, np.moveaxis(arr, axis, -1)), -1, axis)
+
+
+def volume_metrics(nodes, orders, family, form, ids=None):
+    """Returns J (B,n1,n2,n3), Ja (B,3,3,n1,n2,n3) [i, phys], sizes (B,3), coords."""
+    m = [s - 1 for s in nodes.shape[1:4]]
+    for d in range(3):
+        if orders[d] >= 1 and m[d] > orders[d]:
+            raise MeshError(f"mapping order {tuple(m)} exceeds solution order {tuple(orders)}")
+    x = [spectral.rule(int(n), family)[0] for n in orders]
+    w = [spectral.rule(int(n), family)[1] for n in orders]
+    coords = map_points(nodes, *x)
+    if form == "cross":
+        a = map_derivs(nodes, *x)
+        ja = np.stack([np.cross(a[1], a[2]), np.cross(a[2], a[0]), np.cross(a[0], a[1])], axis=1)
+        ja = np.moveaxis(ja, -1, 2)                       # (B, 3[i], 3[n], ...)
+        jac = np.einsum("Eijkx,Eijkx->Eijk", a[0], np.cross(a[1], a[2]))
+        av = a
+    elif form == "curl":
+        D = [spectral.derivative_matrix(xx) for xx in x]
+        # element-local origin: the curl form is translation invariant (the
+        # tensor-product derivatives commute), and local coordinates avoid
+        # multiplying O(1) positions into an O(h^2) result
+        X = coords - coords.reshape(len(coords), -1, 3).mean(axis=1)[:, None, None, None, :]
+        g = [[_coll(X[..., c], k + 1, D[k]) for k in range(3)] for c in range(3)]
+        ja = np.empty((X.shape[0], 3, 3) + X.shape[1:4])
+        for n in range(3):
+            mm, ll = (n + 1) % 3, (n + 2) % 3
+            V = [X[..., ll] * g[mm][k] - X[..., mm] * g[ll][k] for k in range(3)]
+            for i in range(3):
+                j, k = (i + 1) % 3, (i + 2) % 3
+                ja[:, i, n] = -0.5 * (_coll(V[k], j + 1, D[j]) - _coll(V[j], k + 1, D[k]))
+        av = [np.stack([g[c][k] for c in range(3)], axis=-1) for k in range(3)]
+        jac = np.einsum("Eijkx,Eijkx->Eijk", av[0], np.cross(av[1], av[2]))
+    else:
+        raise ValueError(f"unknown metric form {form!r}")
+    if jac.size and np.min(jac) <= 0.0:
+        bad = int(np.argmin(jac.reshape(len(jac), -1).min(axis=1)))
+        e = bad if ids is None else int(ids[bad])
+        raise MeshError(f"inverted element {e}: min Jacobian {np.min(jac):.3e}")
+    www = w[0][:, None, None] * w[1][None, :, None] * w[2][None, None, :]
+    sizes = np.stack([np.einsum("ijk,Eijk->E", www, np.linalg.norm(av[d], axis=-1)) / 4.0
+                      for d in range(3)], axis=1)
+    return jac, ja, sizes, coords
+
+
+def face_dirs(side):
+    d = side // 2
+    t = [k for k in range(3) if k != d]
+    return d, t[0], t[1]
+
+
+def _side_pts(side, p1, p2):
+    d, a, b = face_dirs(side)
+    pts = [None] * 3
+    pts[d] = np.array([-1.0 if side % 2 == 0 else 1.0])
+    pts[a] = np.asarray(p1, float)
+    pts[b] = np.asarray(p2, float)
+    return pts
+
+
+def face_ja_analytic(nodes, side, p1, p2):
+    """Ja^d at face points (t1 x t2 grid): (B, n1, n2, 3)."""
+    d = side // 2
+    a = map_derivs(nodes, *_side_pts(side, p1, p2))
+    j, k = (d + 1) % 3, (d + 2) % 3
+    ja = np.cross(a[j], a[k])
+    return np.take(ja, 0, axis=1 + d)
+
+
+def face_ja_trace(ja_vol, side, orders, family):
+    """Trace of the volume Ja^d polynomial at own face nodes: (B, nt1, nt2, 3)."""
+    d = side // 2
+    row = spectral.bounds(int(orders[d]), family)[side % 2]
+    tr = np.tensordot(ja_vol[:, d], row, axes=([2 + d], [0]))   # (B, 3, nt1, nt2)
+    return np.moveaxis(tr, 1, -1)
+
+
+def face_points(nodes, side, p1, p2):
+    d = side // 2
+    return np.take(map_points(nodes, *_side_pts(side, p1, p2)), 0, axis=1 + d)
+
+
+def sigma_normal(ja_face, side):
+    sign = 1.0 if side % 2 == 1 else -1.0
+    sigma = np.linalg.norm(ja_face, axis=-1)
+    return sigma, sign * ja_face / sigma[..., None]

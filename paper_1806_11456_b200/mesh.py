@@ -376,3 +376,60 @@ def extract_element(msh: HexMesh, e: int) -> HexMesh:
     faces = [Face(0, s, tag=SIDE_NAMES[s]) for s in range(6)]
     faces, tags = _finish_faces(faces)
     return HexMesh(msh.nodes[e : e + 1].copy(), faces, tags, dict(msh.bc))
+
+
+def _proper_rotations():
+    import itertools as it
+    out = []
+    for perm in it.permutations(range(3)):
+        sgn = np.linalg.det(np.eye(3)[list(perm)])
+        for flips in it.product((0, 1), repeat=3):
+            if sgn * (-1) ** sum(flips) > 0:
+                out.append((perm, flips))
+    return out
+
+
+def build_rotated_box(nx: int, ny: int, nz: int, bounds=((0.0, 1.0), (0.0, 1.0), (0.0, 1.0)),
+                      jitter: float = 0.0, seed: int = 0, bc=None) -> HexMesh:
+    """Non-periodic structured box whose elements carry randomly rotated local
+    axes (one of the 24 proper cube rotations each), so that neighbouring
+    faces meet with every orientation code.  Faces come from vertex matching
+    (``faces_from_hexes``); boundary tags are 'boundary'."""
+    rng = np.random.default_rng(seed)
+    (x0, x1), (y0, y1), (z0, z1) = bounds
+    V = np.stack(np.meshgrid(np.linspace(x0, x1, nx + 1), np.linspace(y0, y1, ny + 1),
+                             np.linspace(z0, z1, nz + 1), indexing="ij"), axis=-1)
+    if jitter > 0.0:
+        h = np.array([(x1 - x0) / nx, (y1 - y0) / ny, (z1 - z0) / nz])
+        D = rng.uniform(-jitter, jitter, V.shape) * h
+        D[0, :, :, 0] = D[-1, :, :, 0] = 0.0
+        D[:, 0, :, 1] = D[:, -1, :, 1] = 0.0
+        D[:, :, 0, 2] = D[:, :, -1, 2] = 0.0
+        V = V + D
+    vid = np.arange(V[..., 0].size).reshape(V.shape[:3])
+    flatV = V.reshape(-1, 3)
+    rots = _proper_rotations()
+    nel = nx * ny * nz
+    hexes = np.empty((nel, 2, 2, 2), dtype=np.int64)
+    e = 0
+    for k in range(nz):
+        for j in range(ny):
+            for i in range(nx):
+                base = vid[i:i + 2, j:j + 2, k:k + 2]
+                perm, flips = rots[rng.integers(len(rots))]
+                loc = np.empty((2, 2, 2), dtype=np.int64)
+                for a in (0, 1):
+                    for b in (0, 1):
+                        for c in (0, 1):
+                            new = (a, b, c)
+                            old = [0, 0, 0]
+                            for kk in range(3):
+                                v = new[kk]
+                                old[perm[kk]] = 1 - v if flips[kk] else v
+                            loc[a, b, c] = base[tuple(old)]
+                hexes[e] = loc
+                e += 1
+    corners = flatV[hexes]                                   # (nel, 2, 2, 2, 3)
+    nodes = trilinear_nodes(corners)
+    faces, tags = faces_from_hexes(hexes, lambda e, s: "boundary")
+    return HexMesh(nodes, faces, tags, dict(bc or {}))
