@@ -178,6 +178,26 @@ int tdg_copy_gradient(tdg_plan* plan, double* dst, void* stream);
  * [C][nf] with t1 fastest.  Returns the element count in *len_out. */
 int tdg_debug_copy(tdg_plan* plan, int which, double* dst, int64_t* len_out, void* stream);
 
+/* Per-kernel timing (process-wide): when enabled, every kernel launch made
+ * through this library is bracketed by CUDA events on its own stream.
+ * tdg_timing_read synchronises the recorded events, writes the summed
+ * milliseconds and launch counts per kernel class (TDG_K_*, up to k entries)
+ * and clears the record. */
+#define TDG_K_TRACE 0
+#define TDG_K_SIDE_LIFT 1
+#define TDG_K_FACE_LIFT 2
+#define TDG_K_VOL_LIFT 3
+#define TDG_K_SIDE_FLUX 4
+#define TDG_K_FACE_FLUX 5
+#define TDG_K_VOL_FLUX 6
+#define TDG_K_DT 7
+#define TDG_K_NORM 8
+#define TDG_K_TRANSFER 9
+#define TDG_K_COUNT 10
+int tdg_timing_enable(int on);
+int tdg_timing_read(double* ms, int64_t* counts, int k);
+const char* tdg_kernel_name(int kind);
+
 const char* tdg_last_error(void);
 const char* tdg_version(void);
 

@@ -60,6 +60,9 @@ SIGNATURES = {
     "tdg_prolong_add": ([_VP, _VP, _VP, _VP, _VP], C.c_int),
     "tdg_copy_gradient": ([_VP, _VP, _VP], C.c_int),
     "tdg_debug_copy": ([_VP, C.c_int, _VP, _pi64, _VP], C.c_int),
+    "tdg_timing_enable": ([C.c_int], C.c_int),
+    "tdg_timing_read": ([_pd, _pi64, C.c_int], C.c_int),
+    "tdg_kernel_name": ([C.c_int], C.c_char_p),
     "tdg_last_error": ([], C.c_char_p),
     "tdg_version": ([], C.c_char_p),
 }
@@ -114,3 +117,19 @@ def stream_handle(device=None) -> int:
     import torch
 
     return torch.cuda.current_stream(device).cuda_stream
+
+
+KERNEL_COUNT = 10
+
+
+def timing_enable(on: bool = True):
+    call("tdg_timing_enable", int(bool(on)))
+
+
+def timing_read() -> dict:
+    """{kernel name: (total ms, launches)} since the last read (clears)."""
+    ms = (C.c_double * KERNEL_COUNT)()
+    cnt = (C.c_int64 * KERNEL_COUNT)()
+    call("tdg_timing_read", ms, cnt, KERNEL_COUNT)
+    lib = load()
+    return {lib.tdg_kernel_name(i).decode(): (ms[i], cnt[i]) for i in range(KERNEL_COUNT)}

@@ -74,6 +74,47 @@ struct Allocs {
 int law_nv(int law) { return law == TDG_LAW_NS ? 5 : 1; }
 int law_ngv(int law) { return law == TDG_LAW_NS ? 4 : 1; }
 
+// ---- launch timing -------------------------------------------------------
+struct TimedLaunch {
+  int kind;
+  cudaEvent_t a, b;
+};
+bool g_timing = false;
+std::vector<TimedLaunch> g_launches;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t take_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct KTimer {
+  bool on;
+  TimedLaunch t;
+  cudaStream_t st;
+  KTimer(int kind, cudaStream_t s) : on(g_timing), st(s) {
+    if (!on) return;
+    t.kind = kind;
+    t.a = take_event();
+    t.b = take_event();
+    cudaEventRecord(t.a, st);
+  }
+  ~KTimer() {
+    if (!on) return;
+    cudaEventRecord(t.b, st);
+    g_launches.push_back(t);
+  }
+};
+
+const char* const KNAMES[TDG_K_COUNT] = {"trace_q", "side_lift", "face_lift", "vol_lift", "side_flux",
+                                         "face_flux", "vol_flux", "element_dt", "norm", "transfer"};
+
 __global__ void k_fill(double* p, double v, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -136,13 +177,14 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
   using L = Law<LAW>;
   const DevPlan& d = p->d;
   if (d.nwork == 0) return TDG_OK;
-  k_trace_q<L::NV><<<d.nwork, ELEM_THREADS, 0, st>>>(d, Q);
+  { KTimer kt(TDG_K_TRACE, st); k_trace_q<L::NV><<<d.nwork, ELEM_THREADS, 0, st>>>(d, Q); }
   LAUNCH_CHECK("k_trace_q");
   auto sides = [&](bool flux) -> int {
     const int4* items = isolated ? d.side_iso : d.side_bnd;
     const int n = isolated ? d.nside_iso : d.nside_bnd;
     if (n > 0) {
       const int grid = (n + SIDES_PER_BLOCK - 1) / SIDES_PER_BLOCK;
+      KTimer kt(flux ? TDG_K_SIDE_FLUX : TDG_K_SIDE_LIFT, st);
       if (flux)
         k_side<LAW, true><<<grid, SIDE_THREADS, 0, st>>>(d, items, n);
       else
@@ -150,6 +192,7 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
       LAUNCH_CHECK("k_side");
     }
     if (!isolated && d.nfaces > 0) {
+      KTimer kt(flux ? TDG_K_FACE_FLUX : TDG_K_FACE_LIFT, st);
       if (flux)
         k_face<LAW, true><<<d.nfaces, FACE_THREADS, face_smem_doubles<LAW, true>() * sizeof(double), st>>>(d);
       else
@@ -161,7 +204,7 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
   int rc;
   if (p->viscous) {
     if ((rc = sides(false))) return rc;
-    k_vol_lift<LAW><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q);
+    { KTimer kt(TDG_K_VOL_LIFT, st); k_vol_lift<LAW><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q); }
     LAUNCH_CHECK("k_vol_lift");
   }
   return sides(true);
@@ -172,7 +215,7 @@ int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cuda
   int rc = run_surface<LAW>(p, Q, isolated, st);
   if (rc) return rc;
   if (p->d.nwork == 0) return TDG_OK;
-  k_vol_flux<LAW, MODE><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a);
+  { KTimer kt(TDG_K_VOL_FLUX, st); k_vol_flux<LAW, MODE><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a); }
   LAUNCH_CHECK("k_vol_flux");
   return TDG_OK;
 }
@@ -194,6 +237,34 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 extern "C" {
 
 const char* tdg_last_error(void) { return g_err.c_str(); }
+
+int tdg_timing_enable(int on) {
+  g_timing = on != 0;
+  return TDG_OK;
+}
+
+int tdg_timing_read(double* ms, int64_t* counts, int k) {
+  std::vector<double> acc(TDG_K_COUNT, 0.0);
+  std::vector<int64_t> cnt(TDG_K_COUNT, 0);
+  for (auto& t : g_launches) {
+    cudaError_t e = cudaEventSynchronize(t.b);
+    if (e != cudaSuccess) return fail(TDG_E_CUDA, std::string("timing: ") + cudaGetErrorString(e));
+    float x = 0.f;
+    cudaEventElapsedTime(&x, t.a, t.b);
+    acc[t.kind] += x;
+    cnt[t.kind] += 1;
+    g_event_pool.push_back(t.a);
+    g_event_pool.push_back(t.b);
+  }
+  g_launches.clear();
+  for (int i = 0; i < k && i < TDG_K_COUNT; ++i) {
+    if (ms) ms[i] = acc[i];
+    if (counts) counts[i] = cnt[i];
+  }
+  return TDG_OK;
+}
+
+const char* tdg_kernel_name(int kind) { return (kind >= 0 && kind < TDG_K_COUNT) ? KNAMES[kind] : "?"; }
 const char* tdg_version(void) { return "taudg-b200 0.1.0 sm_100a"; }
 
 int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
@@ -422,6 +493,7 @@ int tdg_element_dt(tdg_plan* p, const double* Q, double cfl_a, double cfl_v, dou
     LAUNCH_CHECK("k_fill");
   }
   if (p->d.nwork == 0) return TDG_OK;
+  KTimer kt(TDG_K_DT, st);
   switch (p->d.law) {
     case TDG_LAW_ADVDIFF:
       k_element_dt<LAW_ADVDIFF><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, Q, cfl_a, cfl_v, dt_slot, dt_min);
@@ -441,6 +513,7 @@ int tdg_norm_inf(tdg_plan* p, const double* X, double* gmax, double* emax, void*
   cudaStream_t st = as_stream(stream);
   if (gmax) CUDA_TRY(cudaMemsetAsync(gmax, 0, sizeof(double), st));
   if (p->d.nwork == 0) return TDG_OK;
+  KTimer kt(TDG_K_NORM, st);
   if (p->nv == 5)
     k_norm<5><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, X, gmax, emax, nullptr);
   else
@@ -577,6 +650,7 @@ int tdg_transfer_destroy(tdg_transfer* t) {
 int tdg_restrict(const tdg_transfer* t, const double* fine, double* coarse, void* stream) {
   if (!t || !fine || !coarse) return fail(TDG_E_ARG, "null argument");
   if (!t->nwork) return TDG_OK;
+  KTimer kt(TDG_K_TRANSFER, as_stream(stream));
   k_transfer<TR_RESTRICT><<<t->nwork, ELEM_THREADS, t->smem, as_stream(stream)>>>(t->d, fine, nullptr, coarse);
   LAUNCH_CHECK("k_transfer(restrict)");
   return TDG_OK;
@@ -585,6 +659,7 @@ int tdg_restrict(const tdg_transfer* t, const double* fine, double* coarse, void
 int tdg_prolong(const tdg_transfer* t, const double* coarse, double* fine, void* stream) {
   if (!t || !fine || !coarse) return fail(TDG_E_ARG, "null argument");
   if (!t->nwork) return TDG_OK;
+  KTimer kt(TDG_K_TRANSFER, as_stream(stream));
   k_transfer<TR_PROLONG><<<t->nwork, ELEM_THREADS, t->smem, as_stream(stream)>>>(t->d, coarse, nullptr, fine);
   LAUNCH_CHECK("k_transfer(prolong)");
   return TDG_OK;
@@ -594,6 +669,7 @@ int tdg_prolong_add(const tdg_transfer* t, const double* Qc, const double* Qc0, 
                     void* stream) {
   if (!t || !fine || !Qc) return fail(TDG_E_ARG, "null argument");
   if (!t->nwork) return TDG_OK;
+  KTimer kt(TDG_K_TRANSFER, as_stream(stream));
   k_transfer<TR_PROLONG_ADD><<<t->nwork, ELEM_THREADS, t->smem, as_stream(stream)>>>(t->d, Qc, Qc0, fine);
   LAUNCH_CHECK("k_transfer(prolong_add)");
   return TDG_OK;
