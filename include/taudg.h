@@ -86,6 +86,18 @@ typedef struct {
   const double* face_geo;      /* [4][(M1+1)(M2+1)] mortar sigma, normal (left parametrisation) */
   int64_t face_geo_len;
 
+  /* per element side (slot*6+side): x = nonconforming-interior | is_right<<1 | orient<<2,
+   * y = M1 | M2<<8 (mortar orders in the left frame), z = face index or -1,
+   * w = offset (nodes) of the side's mortar-order traces when nonconforming */
+  const int32_t* side_info;    /* [nslots*6*4] */
+  int64_t mtr_nodes;           /* total mortar-trace nodes of nonconforming sides */
+  const int64_t* face_m_off;   /* [nfaces] mortar-array offset (nodes), -1 when conforming */
+  int64_t mortar_nodes;        /* total mortar nodes of nonconforming faces */
+  int32_t nup;                 /* up-projection tasks */
+  const int32_t* up;           /* [nup*2] (slot, side) */
+  int32_t ndown;               /* down-projection tasks */
+  const int32_t* down;         /* [ndown*2] (face, is_right) */
+
   int32_t nbfaces;             /* boundary faces */
   const int32_t* bface_info;   /* [nbfaces*4] slot, side, bc kind, 0 */
   const int64_t* ghost_off;    /* [nbfaces] offset (doubles) into ghost, [nv][nf] */
@@ -193,7 +205,9 @@ int tdg_debug_copy(tdg_plan* plan, int which, double* dst, int64_t* len_out, voi
 #define TDG_K_DT 7
 #define TDG_K_NORM 8
 #define TDG_K_TRANSFER 9
-#define TDG_K_COUNT 10
+#define TDG_K_DOWN 10
+#define TDG_K_UP 11
+#define TDG_K_COUNT 12
 int tdg_timing_enable(int on);
 int tdg_timing_read(double* ms, int64_t* counts, int k);
 const char* tdg_kernel_name(int kind);

@@ -27,6 +27,8 @@ class PlanDesc(C.Structure):
         ("side_off", _pi64), ("side_nodes", _i64), ("side_geo", _pd),
         ("nfaces", _i32), ("face_info", _pi32), ("face_geo_off", _pi64), ("face_geo", _pd),
         ("face_geo_len", _i64),
+        ("side_info", _pi32), ("mtr_nodes", _i64), ("face_m_off", _pi64),
+        ("mortar_nodes", _i64), ("nup", _i32), ("up", _pi32), ("ndown", _i32), ("down", _pi32),
         ("nbfaces", _i32), ("bface_info", _pi32), ("ghost_off", _pi64), ("ghost", _pd),
         ("ghost_len", _i64),
     ]
@@ -119,7 +121,7 @@ def stream_handle(device=None) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
-KERNEL_COUNT = 10
+KERNEL_COUNT = 12
 
 
 def timing_enable(on: bool = True):

@@ -113,7 +113,7 @@ struct KTimer {
 };
 
 const char* const KNAMES[TDG_K_COUNT] = {"trace_q", "side_lift", "face_lift", "vol_lift", "side_flux",
-                                         "face_flux", "vol_flux", "element_dt", "norm", "transfer"};
+                                         "face_flux", "vol_flux", "element_dt", "norm", "transfer", "down_proj", "up_proj"};
 
 __global__ void k_fill(double* p, double v, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -147,7 +147,7 @@ namespace {
 
 template <class K>
 int allow_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) {
+  {  // dynamic + static must fit: always raise the dynamic limit to what we launch with
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(bytes));
     if (e != cudaSuccess) return fail(TDG_E_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
@@ -165,8 +165,6 @@ int setup_attrs(tdg_plan* p) {
   if ((rc = allow_smem(k_vol_flux<LAW, MODE_R>, p->smem_flux))) return rc;
   if ((rc = allow_smem(k_vol_flux<LAW, MODE_RK>, p->smem_flux))) return rc;
   if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU>, p->smem_flux))) return rc;
-  if ((rc = allow_smem(k_face<LAW, false>, face_smem_doubles<LAW, false>() * sizeof(double)))) return rc;
-  if ((rc = allow_smem(k_face<LAW, true>, face_smem_doubles<LAW, true>() * sizeof(double)))) return rc;
   (void)sizeof(L);
   return TDG_OK;
 }
@@ -177,8 +175,21 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
   using L = Law<LAW>;
   const DevPlan& d = p->d;
   if (d.nwork == 0) return TDG_OK;
-  { KTimer kt(TDG_K_TRACE, st); k_trace_q<L::NV><<<d.nwork, ELEM_THREADS, 0, st>>>(d, Q); }
+  const int coupled = isolated ? 0 : 1;
+  { KTimer kt(TDG_K_TRACE, st); k_trace_q<L::NV><<<d.nwork, ELEM_THREADS, 0, st>>>(d, Q, coupled); }
   LAUNCH_CHECK("k_trace_q");
+  auto up = [&](bool grad) -> int {
+    if (isolated || d.nup == 0) return TDG_OK;
+    KTimer ku(TDG_K_UP, st);
+    if (grad)
+      k_up<3 * L::NGV><<<(d.nup + 3) / 4, 128, 0, st>>>(d, d.gtr, d.gtrm);
+    else
+      k_up<L::NV><<<(d.nup + 3) / 4, 128, 0, st>>>(d, d.qtr, d.qtrm);
+    LAUNCH_CHECK("k_up");
+    return TDG_OK;
+  };
+  int rc0 = up(false);
+  if (rc0) return rc0;
   auto sides = [&](bool flux) -> int {
     const int4* items = isolated ? d.side_iso : d.side_bnd;
     const int n = isolated ? d.nside_iso : d.nside_bnd;
@@ -194,18 +205,27 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
     if (!isolated && d.nfaces > 0) {
       KTimer kt(flux ? TDG_K_FACE_FLUX : TDG_K_FACE_LIFT, st);
       if (flux)
-        k_face<LAW, true><<<d.nfaces, FACE_THREADS, face_smem_doubles<LAW, true>() * sizeof(double), st>>>(d);
+        k_face<LAW, true><<<d.nfaces, FACE_THREADS, 0, st>>>(d);
       else
-        k_face<LAW, false><<<d.nfaces, FACE_THREADS, face_smem_doubles<LAW, false>() * sizeof(double), st>>>(d);
+        k_face<LAW, false><<<d.nfaces, FACE_THREADS, 0, st>>>(d);
       LAUNCH_CHECK("k_face");
+      if (d.ndown > 0) {
+        KTimer kd(TDG_K_DOWN, st);
+        if (flux)
+          k_down<L::NV><<<(d.ndown + 3) / 4, 128, 0, st>>>(d, d.fsurf);
+        else
+          k_down<3 * L::NGV><<<(d.ndown + 3) / 4, 128, 0, st>>>(d, d.lsurf);
+        LAUNCH_CHECK("k_down");
+      }
     }
     return TDG_OK;
   };
   int rc;
   if (p->viscous) {
     if ((rc = sides(false))) return rc;
-    { KTimer kt(TDG_K_VOL_LIFT, st); k_vol_lift<LAW><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q); }
+    { KTimer kt(TDG_K_VOL_LIFT, st); k_vol_lift<LAW><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q, coupled); }
     LAUNCH_CHECK("k_vol_lift");
+    if ((rc = up(true))) return rc;
   }
   return sides(true);
 }
@@ -320,6 +340,13 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   UP(face_info, desc->face_info, 12 * desc->nfaces);
   UP(face_geo_off, reinterpret_cast<const long long*>(desc->face_geo_off), desc->nfaces);
   UP(face_geo, desc->face_geo, desc->face_geo_len);
+  int* side_info_i;
+  long long* face_m_off;
+  int *down_i, *up_i;
+  UP(side_info_i, desc->side_info, 4 * 6 * ns);
+  UP(up_i, desc->up, 2 * desc->nup);
+  UP(face_m_off, reinterpret_cast<const long long*>(desc->face_m_off), desc->nfaces);
+  UP(down_i, desc->down, 2 * desc->ndown);
   UP(bface_info, desc->bface_info, 4 * desc->nbfaces);
   UP(ghost_off, reinterpret_cast<const long long*>(desc->ghost_off), desc->nbfaces);
   UP(ghost, desc->ghost, desc->ghost_len);
@@ -344,6 +371,12 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.bface_info = bface_info;
   d.ghost_off = ghost_off;
   d.ghost = ghost;
+  d.side_info = reinterpret_cast<const int4*>(side_info_i);
+  d.nup = desc->nup;
+  d.up = reinterpret_cast<const int2*>(up_i);
+  d.face_m_off = face_m_off;
+  d.ndown = desc->ndown;
+  d.down = reinterpret_cast<const int2*>(down_i);
 
   // element work items: runs of identical orders, <= MAXN nodes
   std::vector<int2> work;
@@ -374,13 +407,20 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   if (!rc) rc = p->mem.upload(bnd.data(), bnd.size(), &bnd_d);
   const size_t sn = static_cast<size_t>(desc->side_nodes);
   p->side_nodes = desc->side_nodes;
+
   const int NG = 3 * p->ngv;
-  double *qtr, *lsurf = nullptr, *gtr = nullptr, *fsurf, *grad = nullptr;
+  const size_t tn = static_cast<size_t>(desc->mtr_nodes);
+  const size_t mn = static_cast<size_t>(desc->mortar_nodes);
+  double *qtr, *lsurf = nullptr, *gtr = nullptr, *fsurf, *grad = nullptr, *msurf = nullptr;
+  double *qtrm = nullptr, *gtrm = nullptr;
   if (!rc) rc = p->mem.zeros(sn * p->nv, &qtr);
+  if (!rc) rc = p->mem.zeros(tn * p->nv, &qtrm);
   if (!rc) rc = p->mem.zeros(sn * p->nv, &fsurf);
+  if (!rc) rc = p->mem.zeros(mn * std::max(p->nv, p->viscous ? NG : 1), &msurf);
   if (p->viscous) {
     if (!rc) rc = p->mem.zeros(sn * NG, &lsurf);
     if (!rc) rc = p->mem.zeros(sn * NG, &gtr);
+    if (!rc) rc = p->mem.zeros(tn * NG, &gtrm);
     if (!rc) rc = p->mem.zeros(static_cast<size_t>(p->nodes) * NG, &grad);
   }
   if (rc) {
@@ -394,6 +434,9 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.nside_bnd = static_cast<int>(bnd.size());
   d.side_bnd = bnd_d;
   d.qtr = qtr;
+  d.qtrm = qtrm;
+  d.gtrm = gtrm;
+  d.msurf = msurf;
   d.lsurf = lsurf;
   d.gtr = gtr;
   d.fsurf = fsurf;

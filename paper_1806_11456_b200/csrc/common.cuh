@@ -53,10 +53,22 @@ struct DevPlan {
   const int4* side_iso;      // isolated: every side of every element
   int nside_bnd;
   const int4* side_bnd;      // coupled: boundary faces
+  // per element side (slot*6+side): x = nonconforming-interior | is_right<<1 | orient<<2,
+  // y = M1 | M2<<8 (mortar orders, left frame), z = face index (-1: boundary),
+  // w = mortar-trace offset (nodes) of a nonconforming side
+  const int4* side_info;
+  const long long* face_m_off;   // mortar-surface offset per face (nodes), -1 if conforming
+  int nup;
+  const int2* up;                // (slot, side) up-projection tasks (nonconforming sides)
+  int ndown;
+  const int2* down;              // (face, is_right) down-projection tasks
   // scratch (device)
-  double* qtr;    // [side_nodes][nv]      own-order Q traces
+  double* msurf;  // [mortar_nodes][max(nv, 3*ngv)] mortar surface values (left frame)
+  double* qtrm;   // mortar-order Q traces of nonconforming sides (own frame)
+  double* gtrm;   // mortar-order gradient traces of nonconforming sides
+  double* qtr;    // [side_nodes][nv] own-order Q traces
   double* lsurf;  // [side_nodes][3*ngv]   lift surface contributions
-  double* gtr;    // [side_nodes][3*ngv]   gradient traces
+  double* gtr;    // [side_nodes][3*ngv] own-order gradient traces
   double* fsurf;  // [side_nodes][nv]      flux surface contributions
   double* grad;   // [nodes][3*ngv]        lifted gradient
 };
@@ -108,6 +120,62 @@ __device__ __forceinline__ void block_max_to(double v, double* out, double* red 
     if (lane == 0 && out) atomic_max_nonneg(out, x);
   }
   __syncthreads();
+}
+
+// One warp projects C component arrays of (na x nb) values (a fastest) to
+// (ma x mb):  dst[c][A + ma B] = sum_{a,b} T1[A][a] T2[B][b] src[c][a + na b]
+// (T rows stride 8).  All components are staged together (coalesced loads),
+// then two separable passes; three __syncwarp per call.  s_in/s_tmp hold
+// C*64 doubles each.
+template <int C, class Load, class Store>
+__device__ __forceinline__ void warp_projC(int na, int nb, const double* __restrict__ T1, int ma,
+                                           const double* __restrict__ T2, int mb, double* s_in,
+                                           double* s_tmp, Load ld, Store st) {
+  const int lane = threadIdx.x & 31;
+  // stage: lanes own input positions, loop over components (coalesced per c)
+  const int nin = na * nb;
+  for (int k = lane; k < nin; k += 32) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) s_in[c * 64 + k] = ld(c, k);
+  }
+  __syncwarp();
+  // pass 1 (along a): lanes own (A, b) positions; matrix row cached in registers
+  const int nt = ma * nb;
+  for (int k = lane; k < nt; k += 32) {
+    const int b = k / ma, A = k - b * ma;
+    double r[8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) r[a] = a < na ? T1[A * 8 + a] : 0.0;
+    const int base = na * b;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const double* col = s_in + c * 64 + base;
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+        if (a < na) acc += r[a] * col[a];
+      s_tmp[c * 64 + k] = acc;
+    }
+  }
+  __syncwarp();
+  // pass 2 (along b): lanes own (A, B) output positions
+  const int no = ma * mb;
+  for (int k = lane; k < no; k += 32) {
+    const int B = k / ma, A = k - B * ma;
+    double r[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) r[b] = b < nb ? T2[B * 8 + b] : 0.0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const double* col = s_tmp + c * 64 + A;
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (b < nb) acc += r[b] * col[ma * b];
+      st(c, k, acc);
+    }
+  }
+  __syncwarp();
 }
 
 // face coordinates of a side: normal direction and the two tangential ones

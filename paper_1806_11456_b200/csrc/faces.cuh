@@ -1,13 +1,12 @@
 // faces.cuh — interior-face (mortar) and element-side kernels.
 //
 // Interior faces (operators.py:146-171, 211-217, 251-261, 312-334): both
-// traces are interpolated onto a mortar of order max(own, neighbour) per
-// tangential direction, the numerical flux is evaluated there with the left
-// element's sigma and normal, and flux*sigma is L2-projected back to each
-// side (negated for the right side).  The right trace is re-indexed into the
+// traces live on a mortar of order max(own, neighbour) per tangential
+// direction, the numerical flux is evaluated there with the left element's
+// sigma and normal, and flux*sigma is L2-projected back to each side
+// (negated for the right side).  The right trace is re-indexed into the
 // left's face axes by the face orientation code (3D generalisation of the
-// reference's `flip`).  One 64-thread block per face; the separable 2D
-// projections run through shared memory.
+// reference's `flip`).
 //
 // Side kernels handle physical boundaries (coupled evaluation) and every
 // element side in the isolated evaluation (operators.py:235-249, 294-310).
@@ -25,153 +24,147 @@ __device__ __forceinline__ int right_index(int a, int b, int R1, int R2, int ori
   return (orient & 4) ? (bp + (R2 + 1) * ap) : (ap + (R1 + 1) * bp);
 }
 
-// dst[c][A + ma*B] = sum_{a,b} T1[A][a] T2[B][b] src[c][a + na*b]   (stride 64 per c)
-__device__ __forceinline__ void proj2(const double* src, int na, int nb, const double* T1,
-                                      int ma, const double* T2, int mb, double* tmp, double* dst,
-                                      int C) {
-  for (int u = threadIdx.x; u < C * ma * nb; u += blockDim.x) {
-    const int c = u / (ma * nb), r = u % (ma * nb), A = r % ma, b = r / ma;
-    double acc = 0.0;
-    for (int a = 0; a < na; ++a) acc += T1[A * 8 + a] * src[c * 64 + a + na * b];
-    tmp[c * 64 + A + ma * b] = acc;
-  }
-  __syncthreads();
-  for (int u = threadIdx.x; u < C * ma * mb; u += blockDim.x) {
-    const int c = u / (ma * mb), r = u % (ma * mb), A = r % ma, B = r / ma;
-    double acc = 0.0;
-    for (int b = 0; b < nb; ++b) acc += T2[B * 8 + b] * tmp[c * 64 + A + ma * b];
-    dst[c * 64 + A + ma * B] = acc;
-  }
-  __syncthreads();
-}
-
-template <int LAW, bool FLUX>
-constexpr int face_smem_doubles() {
-  constexpr int NV = Law<LAW>::NV, NG = 3 * Law<LAW>::NGV;
-  constexpr int CIN = FLUX ? NV + NG : NV, COUT = FLUX ? NV : NG;
-  constexpr int CM = CIN > COUT ? CIN : COUT;
-  return 2 * CIN * 64 + 3 * CM * 64 + COUT * 64 + 8 * 64;
-}
-
+// Interior face, pointwise: one thread per mortar node.  Both sides' traces
+// already live at the mortar order (k_trace_q / k_vol_lift interpolate the
+// nonconforming sides), so no shared memory and no barriers are needed.
+// Conforming faces write the signed per-side own-order surface arrays
+// directly; nonconforming faces write one mortar array (left frame) that
+// k_down projects back onto each side (operators.py:211-217, 257-261, 330-334).
 template <int LAW, bool FLUX>
 __global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
-  constexpr int CIN = FLUX ? NV + NG : NV;      // trace components read per side
-  constexpr int COUT = FLUX ? NV : NG;          // surface components written per side
-  constexpr int CM = CIN > COUT ? CIN : COUT;   // mortar / projection buffers hold either
-  extern __shared__ double fsm[];
-  double* inL = fsm;
-  double* inR = inL + CIN * 64;
-  double* mL = inR + CIN * 64;
-  double* mR = mL + CM * 64;
-  double* tmp = mR + CM * 64;
-  double* res = tmp + CM * 64;
-  double(*Tm)[64] = reinterpret_cast<double(*)[64]>(res + COUT * 64);
+  constexpr int COUT = FLUX ? NV : NG;
   const int f = blockIdx.x;
-  const int* fi = P.face_info + 12 * f;
-  const int slotL = fi[0], sideL = fi[1], slotR = fi[2], sideR = fi[3], orient = fi[4];
-  const int L1 = fi[5], L2 = fi[6], R1 = fi[7], R2 = fi[8], M1 = fi[9], M2 = fi[10];
-  const int nL = (L1 + 1) * (L2 + 1), nR = (R1 + 1) * (R2 + 1), nm = (M1 + 1) * (M2 + 1);
-  const bool visc = L::viscous(P.prm);
-  const int cin = (FLUX && visc) ? CIN : NV;
-  const bool conf = (L1 == M1) && (L2 == M2) && (R1 == M1) && (R2 == M2);
-  const long long offL = P.side_off[slotL * 6 + sideL];
-  const long long offR = P.side_off[slotR * 6 + sideR];
-
-  if (!conf) {
-    // up: L->M (dirs 1,2), R->M ; down: M->L, M->R
-    const int fr[8] = {L1, L2, R1, R2, M1, M2, M1, M2};
-    const int to[8] = {M1, M2, M1, M2, L1, L2, R1, R2};
-    for (int u = threadIdx.x; u < 8 * 64; u += blockDim.x) {
-      const int k = u / 64;
-      Tm[k][u % 64] = P.tables[OFF_T + (fr[k] * 8 + to[k]) * 64 + (u % 64)];
-    }
-  }
-  // load traces (left own, right re-indexed into left axes)
-  for (int u = threadIdx.x; u < cin * 64; u += blockDim.x) {
-    const int c = u / 64, k = u % 64;
-    if (k < nL) {
-      inL[u] = (c < NV) ? P.qtr[offL * NV + (long long)c * nL + k]
-                        : P.gtr[offL * NG + (long long)(c - NV) * nL + k];
-    }
-    if (k < nR) {
-      const int a = k % (R1 + 1), b = k / (R1 + 1);
-      const int kr = right_index(a, b, R1, R2, orient);
-      inR[u] = (c < NV) ? P.qtr[offR * NV + (long long)c * nR + kr]
-                        : P.gtr[offR * NG + (long long)(c - NV) * nR + kr];
-    }
-  }
-  __syncthreads();
-  const double* qL = inL;
-  const double* qR = inR;
-  if (!conf) {
-    proj2(inL, L1 + 1, L2 + 1, Tm[0], M1 + 1, Tm[1], M2 + 1, tmp, mL, cin);
-    proj2(inR, R1 + 1, R2 + 1, Tm[2], M1 + 1, Tm[3], M2 + 1, tmp, mR, cin);
-    qL = mL;
-    qR = mR;
-  }
-  // pointwise mortar flux
   const int t = threadIdx.x;
-  if (t < nm) {
-    const double* geo = P.face_geo + P.face_geo_off[f];
-    const double sigma = geo[t];
-    const double nrm[3] = {geo[nm + t], geo[2 * nm + t], geo[3 * nm + t]};
-    double ql[NV], qr[NV];
+  const int* fi = P.face_info + 12 * f;
+  const int M1 = fi[9], M2 = fi[10];
+  const int nm = (M1 + 1) * (M2 + 1);
+  if (t >= nm) return;
+  const int slotL = fi[0], sideL = fi[1], slotR = fi[2], sideR = fi[3], orient = fi[4];
+  const int L1 = fi[5], L2 = fi[6], R1 = fi[7], R2 = fi[8];
+  const bool conf = (L1 == M1) && (L2 == M2) && (R1 == M1) && (R2 == M2);
+  const int A = t % (M1 + 1), B = t / (M1 + 1);
+  const int kR = right_index(A, B, M1, M2, orient);
+  // conforming: own-order traces; nonconforming: mortar traces from k_up
+  const double* qsrc = conf ? P.qtr : P.qtrm;
+  const double* gsrc = conf ? P.gtr : P.gtrm;
+  const long long tL = conf ? P.side_off[slotL * 6 + sideL] : P.side_info[slotL * 6 + sideL].w;
+  const long long tR = conf ? P.side_off[slotR * 6 + sideR] : P.side_info[slotR * 6 + sideR].w;
+  const double* geo = P.face_geo + P.face_geo_off[f];
+  const double sigma = geo[t];
+  const double nrm[3] = {geo[nm + t], geo[2 * nm + t], geo[3 * nm + t]};
+  double ql[NV], qr[NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      ql[v] = qL[v * 64 + t];
-      qr[v] = qR[v * 64 + t];
-    }
-    if (!FLUX) {
-      double gl[NGV], gr[NGV];
-      L::grad_vars(P.prm, ql, gl);
-      L::grad_vars(P.prm, qr, gr);
+  for (int v = 0; v < NV; ++v) {
+    ql[v] = qsrc[tL * NV + (long long)v * nm + t];
+    qr[v] = qsrc[tR * NV + (long long)v * nm + kR];
+  }
+  double val[COUT];
+  if (!FLUX) {
+    double gl[NGV], gr[NGV];
+    L::grad_vars(P.prm, ql, gl);
+    L::grad_vars(P.prm, qr, gr);
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int k = 0; k < NGV; ++k) val[d * NGV + k] = 0.5 * (gl[k] + gr[k]) * nrm[d] * sigma;
+  } else {
+    double F[NV];
+    L::riemann(P.prm, ql, qr, nrm, F);
+    if (L::viscous(P.prm)) {
+      double GL[3][NGV], GR[3][NGV], fl[NV], fr[NV];
 #pragma unroll
       for (int d = 0; d < 3; ++d)
 #pragma unroll
-        for (int k = 0; k < NGV; ++k)
-          res[(d * NGV + k) * 64 + t] = 0.5 * (gl[k] + gr[k]) * nrm[d] * sigma;
-    } else {
-      double F[NV];
-      L::riemann(P.prm, ql, qr, nrm, F);
-      if (visc) {
-        double GL[3][NGV], GR[3][NGV], fl[NV], fr2[NV];
+        for (int k = 0; k < NGV; ++k) {
+          GL[d][k] = gsrc[tL * NG + (long long)(d * NGV + k) * nm + t];
+          GR[d][k] = gsrc[tR * NG + (long long)(d * NGV + k) * nm + kR];
+        }
+      L::visc_normal(P.prm, ql, GL, nrm, fl);
+      L::visc_normal(P.prm, qr, GR, nrm, fr);
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int k = 0; k < NGV; ++k) {
-            GL[d][k] = qL[(NV + d * NGV + k) * 64 + t];
-            GR[d][k] = qR[(NV + d * NGV + k) * 64 + t];
-          }
-        L::visc_normal(P.prm, ql, GL, nrm, fl);
-        L::visc_normal(P.prm, qr, GR, nrm, fr2);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) F[v] -= 0.5 * (fl[v] + fr2[v]);
-      }
-#pragma unroll
-      for (int v = 0; v < NV; ++v) res[v * 64 + t] = F[v] * sigma;
+      for (int v = 0; v < NV; ++v) F[v] -= 0.5 * (fl[v] + fr[v]);
     }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) val[v] = F[v] * sigma;
   }
-  __syncthreads();
-  const double* oL = res;
-  const double* oR = res;
-  if (!conf) {
-    proj2(res, M1 + 1, M2 + 1, Tm[4], L1 + 1, Tm[5], L2 + 1, tmp, mL, COUT);
-    proj2(res, M1 + 1, M2 + 1, Tm[6], R1 + 1, Tm[7], R2 + 1, tmp, mR, COUT);
-    oL = mL;
-    oR = mR;
-  }
-  double* dst = FLUX ? P.fsurf : P.lsurf;
-  for (int u = threadIdx.x; u < COUT * 64; u += blockDim.x) {
-    const int c = u / 64, k = u % 64;
-    if (k < nL) dst[offL * COUT + (long long)c * nL + k] = oL[u];
-    if (k < nR) {
-      const int a = k % (R1 + 1), b = k / (R1 + 1);
-      const int kr = right_index(a, b, R1, R2, orient);
-      dst[offR * COUT + (long long)c * nR + kr] = -oR[u];
+  if (conf) {
+    double* dst = FLUX ? P.fsurf : P.lsurf;
+    const long long oL = P.side_off[slotL * 6 + sideL] * COUT;
+    const long long oR = P.side_off[slotR * 6 + sideR] * COUT;
+#pragma unroll
+    for (int c = 0; c < COUT; ++c) {
+      dst[oL + (long long)c * nm + t] = val[c];
+      dst[oR + (long long)c * nm + kR] = -val[c];
     }
+  } else {
+    double* dst = P.msurf + P.face_m_off[f] * COUT;
+#pragma unroll
+    for (int c = 0; c < COUT; ++c) dst[(long long)c * nm + t] = val[c];
   }
+}
+
+// Mortar interpolation of a nonconforming side's own-order traces (own frame):
+// one warp per side, all C components at once (warp_projC).
+template <int C>
+__global__ void __launch_bounds__(128) k_up(DevPlan P, const double* __restrict__ own,
+                                           double* __restrict__ mort) {
+  __shared__ double scr[4][2][C * 64];
+  const int warp = threadIdx.x >> 5;
+  const int task = blockIdx.x * 4 + warp;
+  if (task >= P.nup) return;
+  const int2 tk = P.up[task];
+  const int slot = tk.x, s = tk.y;
+  const int4 si = P.side_info[slot * 6 + s];
+  const int* od = P.orders + 3 * slot;
+  int d, a, b;
+  side_dirs(s, d, a, b);
+  const int na = od[a] + 1, nb = od[b] + 1, nf = na * nb;
+  const int M1 = si.y & 255, M2 = (si.y >> 8) & 255;
+  const bool swap_r = (si.x & 2) && (((si.x >> 2) & 7) & 4);
+  const int ma = (swap_r ? M2 : M1) + 1, mb = (swap_r ? M1 : M2) + 1, nm = ma * mb;
+  const double* T1 = P.tables + OFF_T + ((na - 1) * 8 + (ma - 1)) * 64;
+  const double* T2 = P.tables + OFF_T + ((nb - 1) * 8 + (mb - 1)) * 64;
+  const double* src = own + P.side_off[slot * 6 + s] * C;
+  double* dst = mort + (long long)si.w * C;
+  warp_projC<C>(na, nb, T1, ma, T2, mb, scr[warp][0], scr[warp][1],
+                [&](int c, int k) { return src[(long long)c * nf + k]; },
+                [&](int c, int k, double x) { dst[(long long)c * nm + k] = x; });
+}
+
+// L2 projection of a nonconforming face's mortar values back onto one side
+// (left or right, own order; the right side negated and re-oriented): one
+// warp per (face, side), all components at once (warp_projC).
+template <int C>
+__global__ void __launch_bounds__(128) k_down(DevPlan P, double* __restrict__ dst) {
+  __shared__ double scr[4][2][C * 64];
+  const int warp = threadIdx.x >> 5;
+  const int task = blockIdx.x * 4 + warp;
+  if (task >= P.ndown) return;
+  const int2 dt = P.down[task];
+  const int* fi = P.face_info + 12 * dt.x;
+  const int M1 = fi[9], M2 = fi[10], orient = fi[4];
+  const int nm = (M1 + 1) * (M2 + 1);
+  const double* src = P.msurf + P.face_m_off[dt.x] * C;
+  const bool right = dt.y != 0;
+  const int o1 = right ? fi[7] : fi[5], o2 = right ? fi[8] : fi[6];   // aligned own orders
+  const int slot = right ? fi[2] : fi[0], side = right ? fi[3] : fi[1];
+  const double* T1 = P.tables + OFF_T + (M1 * 8 + o1) * 64;
+  const double* T2 = P.tables + OFF_T + (M2 * 8 + o2) * 64;
+  const int nf = (o1 + 1) * (o2 + 1);
+  double* out = dst + P.side_off[slot * 6 + side] * C;
+  if (!right)
+    warp_projC<C>(M1 + 1, M2 + 1, T1, o1 + 1, T2, o2 + 1, scr[warp][0], scr[warp][1],
+                  [&](int c, int k) { return src[(long long)c * nm + k]; },
+                  [&](int c, int k, double x) { out[(long long)c * nf + k] = x; });
+  else
+    warp_projC<C>(M1 + 1, M2 + 1, T1, o1 + 1, T2, o2 + 1, scr[warp][0], scr[warp][1],
+                  [&](int c, int k) { return src[(long long)c * nm + k]; },
+                  [&](int c, int k, double x) {
+                    const int a = k % (o1 + 1), b = k / (o1 + 1);
+                    out[(long long)c * nf + right_index(a, b, o1, o2, orient)] = -x;
+                  });
 }
 
 // Side kernel: item = (slot, side, kind [-1 = isolated], ghost offset).
@@ -191,12 +184,13 @@ __global__ void __launch_bounds__(SIDE_THREADS) k_side(DevPlan P, const int4* __
   const int nf = (od[a] + 1) * (od[b] + 1);
   if (kf >= nf) return;
   const long long so = P.side_off[slot * 6 + side];
+  const long long to = so;   // own-order traces
   const double* geo = P.side_geo + so * 4;
   const double sigma = geo[kf];
   const double nrm[3] = {geo[nf + kf], geo[2 * nf + kf], geo[3 * nf + kf]};
   double q[NV];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) q[v] = P.qtr[so * NV + (long long)v * nf + kf];
+  for (int v = 0; v < NV; ++v) q[v] = P.qtr[to * NV + (long long)v * nf + kf];
   double gh[NV];
   if (kind >= 0) {
     // ghost offset (doubles); negative: the BC needs no ghost array
@@ -228,7 +222,7 @@ __global__ void __launch_bounds__(SIDE_THREADS) k_side(DevPlan P, const int4* __
 #pragma unroll
       for (int dd = 0; dd < 3; ++dd)
 #pragma unroll
-        for (int k = 0; k < NGV; ++k) G[dd][k] = P.gtr[so * NG + (long long)(dd * NGV + k) * nf + kf];
+        for (int k = 0; k < NGV; ++k) G[dd][k] = P.gtr[to * NG + (long long)(dd * NGV + k) * nf + kf];
     }
     if (kind < 0) {
       double f[3][NV];

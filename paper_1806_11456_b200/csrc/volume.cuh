@@ -46,9 +46,55 @@ __device__ __forceinline__ const double* metric_ptr(const DevPlan& P, int slot, 
 }
 
 // ---------------------------------------------------------------------------
-// Q traces on the six sides at own order (operators.py:73-80, 185-194)
+// Side traces (operators.py:73-80, 185-194).  One warp per element side: the
+// own-order trace (LGL: gather of the face nodes; LG: boundary-row
+// contraction) is written as is, or — for nonconforming interior sides of a
+// coupled evaluation — interpolated onto the side's mortar (own frame)
+// through warp_proj2, so the face kernels are pointwise.
+
+__device__ __forceinline__ void side_mortar_dims(int4 si, int& ma, int& mb) {
+  const int M1 = si.y & 255, M2 = (si.y >> 8) & 255;
+  const bool swap_r = (si.x & 2) && (((si.x >> 2) & 7) & 4);
+  ma = (swap_r ? M2 : M1) + 1;
+  mb = (swap_r ? M1 : M2) + 1;
+}
+
+// Own-order side traces of C components for every side of a work item; one
+// warp per side, lanes over face nodes (coalesced).  vol(e, c, off) reads the
+// element volume array.
+template <class Vol>
+__device__ __forceinline__ void item_side_traces(const DevPlan& P, int slot0, int E, const int np[3],
+                                                 const int strides[3], const double (*bnd)[16],
+                                                 int C, double* buf, Vol vol) {
+  const bool lgl = P.family == 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int task = warp; task < E * 6; task += ELEM_THREADS / 32) {
+    const int e = task / 6, s = task % 6, slot = slot0 + e;
+    int d, a, b;
+    side_dirs(s, d, a, b);
+    const int na = np[a], nf = na * np[b];
+    const int last = (s & 1) ? (np[d] - 1) * strides[d] : 0;
+    const double* row = &bnd[d][(s & 1) * 8];
+    double* dst = buf + P.side_off[slot * 6 + s] * C;
+    for (int k = lane; k < nf; k += 32) {
+      const int off0 = (k % na) * strides[a] + (k / na) * strides[b];
+      for (int c = 0; c < C; ++c) {
+        double acc;
+        if (lgl) {
+          acc = vol(e, c, off0 + last);
+        } else {
+          acc = 0.0;
+          for (int m = 0; m < np[d]; ++m) acc += row[m] * vol(e, c, off0 + m * strides[d]);
+        }
+        dst[(long long)c * nf + k] = acc;
+      }
+    }
+  }
+}
+
 template <int NV>
-__global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const double* __restrict__ Q) {
+__global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const double* __restrict__ Q,
+                                                          int coupled) {
   __shared__ double sb[3][16];
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.orders + 3 * wi.x;
@@ -59,40 +105,17 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
   const int np[3] = {No[0] + 1, No[1] + 1, No[2] + 1};
   const int n = np[0] * np[1] * np[2];
   const int strides[3] = {1, np[0], np[0] * np[1]};
-  const int items = wi.y * 6 * 64;
-  const bool lgl = P.family == 1;
-  for (int u = threadIdx.x; u < items; u += blockDim.x) {
-    const int e = u / 384, s = (u / 64) % 6, kf = u % 64;
-    int d, a, b;
-    side_dirs(s, d, a, b);
-    const int nf = np[a] * np[b];
-    if (kf >= nf) continue;
-    const int ia = kf % np[a], ib = kf / np[a];
-    const int slot = wi.x + e;
-    const long long base = P.node_off[slot] * NV;
-    const long long so = P.side_off[slot * 6 + s];
-    const int off0 = ia * strides[a] + ib * strides[b];
-    const double* row = &sb[d][(s & 1) * 8];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const double* qv = Q + base + (long long)v * n + off0;
-      double acc;
-      if (lgl) {
-        acc = qv[(s & 1) ? (np[d] - 1) * strides[d] : 0];
-      } else {
-        acc = 0.0;
-        for (int m = 0; m < np[d]; ++m) acc += row[m] * qv[m * strides[d]];
-      }
-      P.qtr[so * NV + (long long)v * nf + kf] = acc;
-    }
-  }
+  (void)coupled;
+  item_side_traces(P, wi.x, wi.y, np, strides, sb, NV, P.qtr,
+                   [&](int e, int c, int off) { return Q[(P.node_off[wi.x + e] * NV) + (long long)c * n + off]; });
 }
 
 // ---------------------------------------------------------------------------
 // BR1 lift, volume part + scatter of the face contributions, times M^-1
 // (operators.py:224-265); writes the gradient and its side traces.
 template <int LAW>
-__global__ void __launch_bounds__(ELEM_THREADS) k_vol_lift(DevPlan P, const double* __restrict__ Q) {
+__global__ void __launch_bounds__(ELEM_THREADS) k_vol_lift(DevPlan P, const double* __restrict__ Q,
+                                                          int coupled) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
@@ -218,26 +241,13 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_vol_lift(DevPlan P, const doub
     }
   }
   __syncthreads();
-  // gradient traces on the six sides
-  const int np[3] = {n1p, n2p, n3p};
-  const int strides[3] = {1, n1p, n1p * n2p};
-  const int items = wi.y * 6 * 64;
-  for (int u = threadIdx.x; u < items; u += blockDim.x) {
-    const int e = u / 384, s = (u / 64) % 6, kf = u % 64;
-    int d, a, b;
-    side_dirs(s, d, a, b);
-    const int nf = np[a] * np[b];
-    if (kf >= nf) continue;
-    const int ia = kf % np[a], ib = kf / np[a];
-    const int slot = wi.x + e;
-    const long long so = P.side_off[slot * 6 + s];
-    const int off0 = e * n + ia * strides[a] + ib * strides[b];
-    const double* row = &T.bnd[d][(s & 1) * 8];
-    for (int c = 0; c < NG; ++c) {
-      double acc = 0.0;
-      for (int m = 0; m < np[d]; ++m) acc += row[m] * G[c * tot + off0 + m * strides[d]];
-      P.gtr[so * NG + (long long)c * nf + kf] = acc;
-    }
+  // gradient traces on the six sides (own order, or mortar order when nonconforming)
+  {
+    const int np[3] = {n1p, n2p, n3p};
+    const int strides[3] = {1, n1p, n1p * n2p};
+    (void)coupled;
+    item_side_traces(P, wi.x, wi.y, np, strides, T.bnd, NG, P.gtr,
+                     [&](int e, int c, int off) { return G[c * tot + e * n + off]; });
   }
 }
 

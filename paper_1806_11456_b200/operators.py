@@ -215,6 +215,42 @@ class DGOperator:
             geo_off[ks] = goff + np.arange(len(ks)) * 4 * nm
             goff += len(ks) * 4 * nm
             geo_chunks.append(vals.ravel())
+        # per-side mortar bookkeeping (traces at mortar order on nonconforming sides)
+        ns = of.num_elements
+        side_info = np.zeros((ns, 6, 4), np.int32)
+        side_info[:, :, 2] = -1
+        mcap = np.zeros((ns, 6), np.int64)
+        face_m_off = np.full(len(idx_int), -1, np.int64)
+        down = []
+        moff = 0
+        if len(info):
+            conf = ((info[:, 5] == info[:, 9]) & (info[:, 6] == info[:, 10])
+                    & (info[:, 7] == info[:, 9]) & (info[:, 8] == info[:, 10]))
+            nm = (info[:, 9] + 1) * (info[:, 10] + 1)
+            packed_m = info[:, 9] | (info[:, 10] << 8)
+            for side_col, slot_col, right in ((1, 0, 0), (3, 2, 1)):
+                sl, sd = info[:, slot_col], info[:, side_col]
+                side_info[sl, sd, 0] = (~conf).astype(np.int32) | (right << 1) | (info[:, 4] << 2)
+                side_info[sl, sd, 1] = packed_m
+                side_info[sl, sd, 2] = np.arange(len(info))
+                mcap[sl, sd] = np.where(conf, 0, nm)
+            nc = np.flatnonzero(~conf)
+            face_m_off[nc] = np.concatenate([[0], np.cumsum(nm[nc])])[:-1]
+            moff = int(nm[nc].sum())
+            down = np.stack([np.repeat(nc, 2), np.tile([0, 1], len(nc))], axis=1)
+        moffs = np.concatenate([[0], np.cumsum(mcap.ravel())])[:-1].reshape(ns, 6)
+        if moffs.size and moffs.max() >= 2 ** 31:
+            raise ConfigError("mortar trace offsets exceed 32 bits")
+        side_info[:, :, 3] = np.where(mcap > 0, moffs, -1)
+        up = np.argwhere(mcap > 0)
+        self._side_info = _as(side_info.ravel(), np.int32)
+        self._mtr_nodes = int(mcap.sum())
+        self._up = _as(up.ravel() if len(up) else np.zeros(2, np.int32), np.int32)
+        self._nup = len(up)
+        self._face_m_off = _as(face_m_off if len(face_m_off) else np.zeros(1, np.int64), np.int64)
+        self._mortar_nodes = moff
+        self._down = _as(np.asarray(down).ravel() if len(down) else np.zeros(2, np.int32), np.int32)
+        self._ndown = len(down)
         self._face_info = _as(info.ravel() if len(info) else np.zeros(12, np.int32), np.int32)
         self._nfaces = len(idx_int)
         self._face_geo_off = _as(geo_off if len(geo_off) else np.zeros(1, np.int64), np.int64)
@@ -299,6 +335,14 @@ class DGOperator:
         d.face_info = _p(self._face_info, C.c_int32)
         d.face_geo_off = _p(self._face_geo_off, C.c_int64)
         d.face_geo, d.face_geo_len = _p(self._face_geo, C.c_double), len(self._face_geo)
+        d.side_info = _p(self._side_info, C.c_int32)
+        d.mtr_nodes = self._mtr_nodes
+        d.nup = self._nup
+        d.up = _p(self._up, C.c_int32)
+        d.face_m_off = _p(self._face_m_off, C.c_int64)
+        d.mortar_nodes = self._mortar_nodes
+        d.ndown = self._ndown
+        d.down = _p(self._down, C.c_int32)
         d.nbfaces = self._nbfaces
         d.bface_info = _p(self._bface_info, C.c_int32)
         d.ghost_off = _p(self._ghost_off, C.c_int64)
