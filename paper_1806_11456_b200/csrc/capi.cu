@@ -178,18 +178,7 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
   const int coupled = isolated ? 0 : 1;
   { KTimer kt(TDG_K_TRACE, st); k_trace_q<L::NV><<<d.nwork, ELEM_THREADS, 0, st>>>(d, Q, coupled); }
   LAUNCH_CHECK("k_trace_q");
-  auto up = [&](bool grad) -> int {
-    if (isolated || d.nup == 0) return TDG_OK;
-    KTimer ku(TDG_K_UP, st);
-    if (grad)
-      k_up<3 * L::NGV><<<(d.nup + 3) / 4, 128, 0, st>>>(d, d.gtr, d.gtrm);
-    else
-      k_up<L::NV><<<(d.nup + 3) / 4, 128, 0, st>>>(d, d.qtr, d.qtrm);
-    LAUNCH_CHECK("k_up");
-    return TDG_OK;
-  };
-  int rc0 = up(false);
-  if (rc0) return rc0;
+
   auto sides = [&](bool flux) -> int {
     const int4* items = isolated ? d.side_iso : d.side_bnd;
     const int n = isolated ? d.nside_iso : d.nside_bnd;
@@ -225,7 +214,6 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
     if ((rc = sides(false))) return rc;
     { KTimer kt(TDG_K_VOL_LIFT, st); k_vol_lift<LAW><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q, coupled); }
     LAUNCH_CHECK("k_vol_lift");
-    if ((rc = up(true))) return rc;
   }
   return sides(true);
 }
