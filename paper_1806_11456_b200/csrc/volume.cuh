@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
 // BR1 lift, volume part + scatter of the face contributions, times M^-1
 // (operators.py:224-265); writes the gradient and its side traces.
 template <int LAW>
-__global__ void __launch_bounds__(ELEM_THREADS) k_vol_lift(DevPlan P, const double* __restrict__ Q,
+__global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const double* __restrict__ Q,
                                                           int coupled) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_vol_lift(DevPlan P, const doub
   double* js = sm + NGV * tot;   // [9][tot]
   __syncthreads();
 
-#pragma unroll
+#pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
     const int t = threadIdx.x + r * ELEM_THREADS;
     if (t < tot) {
@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_vol_lift(DevPlan P, const doub
   __syncthreads();
   // gradient traces on the six sides (own order, or mortar order when nonconforming)
   {
-    constexpr int CH = NG < 4 ? NG : 4;
+    constexpr int CH = NG < 2 ? NG : 2;
     __shared__ double scratch[ELEM_THREADS / 32 * 2 * CH * 64];
     const int np[3] = {n1p, n2p, n3p};
     const int strides[3] = {1, n1p, n1p * n2p};
@@ -293,7 +293,7 @@ struct FluxArgs {
 };
 
 template <int LAW, int MODE>
-__global__ void __launch_bounds__(ELEM_THREADS) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
+__global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_vol_flux(DevPlan P, const doub
   double* ft = sm;   // [3][NV][tot]
   __syncthreads();
 
-#pragma unroll
+#pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
     const int t = threadIdx.x + r * ELEM_THREADS;
     if (t < tot) {
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_vol_flux(DevPlan P, const doub
   __syncthreads();
 
   double rmax = 0.0;
-#pragma unroll
+#pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
     const int t = threadIdx.x + r * ELEM_THREADS;
     if (t < tot) {
