@@ -42,6 +42,17 @@ def _dist():
     return ws, rank, local
 
 
+def max_over_ranks(x, dist=None, device="cpu"):
+    """Max of a per-rank float over all ranks (timing rule: max over ranks)."""
+    if dist is None or not dist.is_initialized():
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def _peak_hbm():
     try:
         with open(PEAKS_PATH) as fh:
@@ -197,11 +208,7 @@ def run_b200(args):
             dist.barrier()
 
     def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return globals()["max_over_ranks"](x, dist, "cuda")
 
     # ---- residual throughput, config 3 -------------------------------------
     t_setup = time.perf_counter()

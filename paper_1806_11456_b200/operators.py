@@ -356,10 +356,13 @@ class DGOperator:
         return self.__dict__["_moff"]
 
     def __del__(self):
-        plan = getattr(self, "_plan", None)
-        if plan is not None and _lib._lib is not None:
-            _lib._lib.tdg_plan_destroy(plan)
-            self._plan = None
+        try:
+            plan = getattr(self, "_plan", None)
+            if plan is not None and _lib._lib is not None:
+                _lib._lib.tdg_plan_destroy(plan)
+                self._plan = None
+        except Exception:  # interpreter shutdown: module globals may be gone
+            pass
 
     # --- helpers -----------------------------------------------------------------
     @property
