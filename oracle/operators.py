@@ -376,6 +376,22 @@ class DGOperator:
     def truncation(self, Q, isolated=False):
         return self.truncation_from_avalue(self.m_inv_apply(Q, isolated=isolated))
 
+    def term_scale(self, Q, isolated=False):
+        """max |WD(f~)| over nodes: the magnitude of the terms that cancel in
+        F for near-freestream states — the normaliser for round-off-level
+        parity of F, r and tau."""
+        law = self.law
+        G = self._lift_gradient(Q, self._traces(Q.blocks), isolated) if law.viscous else None
+        out = 0.0
+        for g, go in enumerate(self.group_ops):
+            q = Q.blocks[g]
+            f = law.adv_flux(q)
+            if G is not None:
+                f = f - law.visc_flux(q, G[g])
+            ft = np.einsum("bidxyz,bdvxyz->bivxyz", go.ja, f)
+            out = max(out, float(np.abs(self._weak_div(g, ft)).max()))
+        return out
+
     def gradient(self, Q, isolated=False):
         """Lifted gradient blocks (B, 3, ngv, ...) — exposed for kernel parity."""
         return self._lift_gradient(Q, self._traces(Q.blocks), isolated)
