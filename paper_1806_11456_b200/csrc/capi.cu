@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -133,6 +134,7 @@ struct tdg_plan {
   std::vector<long long> node_off_h;
   size_t smem_lift = 0, smem_flux = 0;
   int64_t side_nodes = 0;
+  int iso = -1;          // isotropic order of a single-bucket plan, else -1
 };
 
 struct tdg_transfer {
@@ -155,18 +157,38 @@ int allow_smem(K kernel, size_t bytes) {
   return TDG_OK;
 }
 
+// compile-time isotropic order for single-bucket Navier-Stokes plans
+template <int LAW, class F>
+int with_nx(int iso, F&& f) {
+  if (LAW == LAW_NS) {
+    switch (iso) {
+      case 1: return f(std::integral_constant<int, 1>());
+      case 2: return f(std::integral_constant<int, 2>());
+      case 3: return f(std::integral_constant<int, 3>());
+      case 4: return f(std::integral_constant<int, 4>());
+      case 5: return f(std::integral_constant<int, 5>());
+      case 6: return f(std::integral_constant<int, 6>());
+      case 7: return f(std::integral_constant<int, 7>());
+      default: break;
+    }
+  }
+  return f(std::integral_constant<int, -1>());
+}
+
 template <int LAW>
 int setup_attrs(tdg_plan* p) {
   using L = Law<LAW>;
-  int rc;
-  if ((rc = allow_smem(k_vol_lift<LAW>, p->smem_lift))) return rc;
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F>, p->smem_flux))) return rc;
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_A>, p->smem_flux))) return rc;
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_R>, p->smem_flux))) return rc;
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_RK>, p->smem_flux))) return rc;
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU>, p->smem_flux))) return rc;
-  (void)sizeof(L);
-  return TDG_OK;
+  return with_nx<LAW>(p->iso, [&](auto nx) -> int {
+    constexpr int NX = decltype(nx)::value;
+    int rc;
+    if ((rc = allow_smem(k_vol_lift<LAW, NX>, p->smem_lift))) return rc;
+    if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, NX>, p->smem_flux))) return rc;
+    if ((rc = allow_smem(k_vol_flux<LAW, MODE_A, NX>, p->smem_flux))) return rc;
+    if ((rc = allow_smem(k_vol_flux<LAW, MODE_R, NX>, p->smem_flux))) return rc;
+    if ((rc = allow_smem(k_vol_flux<LAW, MODE_RK, NX>, p->smem_flux))) return rc;
+    if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, NX>, p->smem_flux))) return rc;
+    return TDG_OK;
+  });
 }
 
 // trace -> lift (if viscous) -> face fluxes; leaves fsurf ready for k_vol_flux
@@ -212,7 +234,13 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
   int rc;
   if (p->viscous) {
     if ((rc = sides(false))) return rc;
-    { KTimer kt(TDG_K_VOL_LIFT, st); k_vol_lift<LAW><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q, coupled); }
+    {
+      KTimer kt(TDG_K_VOL_LIFT, st);
+      with_nx<LAW>(p->iso, [&](auto nx) -> int {
+        k_vol_lift<LAW, decltype(nx)::value><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q, coupled);
+        return 0;
+      });
+    }
     LAUNCH_CHECK("k_vol_lift");
   }
   return sides(true);
@@ -223,7 +251,13 @@ int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cuda
   int rc = run_surface<LAW>(p, Q, isolated, st);
   if (rc) return rc;
   if (p->d.nwork == 0) return TDG_OK;
-  { KTimer kt(TDG_K_VOL_FLUX, st); k_vol_flux<LAW, MODE><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a); }
+  {
+    KTimer kt(TDG_K_VOL_FLUX, st);
+    with_nx<LAW>(p->iso, [&](auto nx) -> int {
+      k_vol_flux<LAW, MODE, decltype(nx)::value><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a);
+      return 0;
+    });
+  }
   LAUNCH_CHECK("k_vol_flux");
   return TDG_OK;
 }
@@ -366,6 +400,13 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.ndown = desc->ndown;
   d.down = reinterpret_cast<const int2*>(down_i);
 
+  {
+    int iso = ns > 0 ? p->orders_h[0] : -1;
+    for (int s = 0; s < ns && iso >= 0; ++s)
+      for (int dd = 0; dd < 3; ++dd)
+        if (p->orders_h[3 * s + dd] != iso) iso = -1;
+    p->iso = iso;
+  }
   // element work items: runs of identical orders, <= MAXN nodes
   std::vector<int2> work;
   for (int s = 0; s < ns;) {

@@ -136,22 +136,34 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
 // ---------------------------------------------------------------------------
 // BR1 lift, volume part + scatter of the face contributions, times M^-1
 // (operators.py:224-265); writes the gradient and its side traces.
-template <int LAW>
+//
+// NX >= 0: compile-time isotropic order (the plan is one (NX,NX,NX) bucket),
+// so index math folds and the contractions unroll; NX = -1: runtime orders.
+// Work items whose elements are all affine take the reference-gradient path:
+// -sum_i Ja^i_d WD_i(g) with the element's constant Ja (no per-node metrics).
+template <int LAW, int NX>
 __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const double* __restrict__ Q,
                                                           int coupled) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
+  __shared__ int s_aff;
   extern __shared__ double sm[];
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.orders + 3 * wi.x;
-  const int N1 = od[0], N2 = od[1], N3 = od[2];
+  const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
   load_tables(P, N1, N2, N3, T);
+  if (threadIdx.x == 0) {
+    int a = 1;
+    for (int e = 0; e < wi.y; ++e) a &= P.affine[wi.x + e] != 0;
+    s_aff = a;
+  }
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
   double* gs = sm;               // [NGV][tot]
-  double* js = sm + NGV * tot;   // [9][tot]
+  double* js = sm + NGV * tot;   // [9][tot]  (curved items only)
   __syncthreads();
+  const bool aff = s_aff != 0;
 
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
@@ -165,10 +177,12 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
       L::grad_vars(P.prm, q, g);
 #pragma unroll
       for (int k = 0; k < NGV; ++k) gs[k * tot + t] = g[k];
-      int ms;
-      const double* m = metric_ptr(P, slot, node, n, ms);
+      if (!aff) {
+        int ms;
+        const double* m = metric_ptr(P, slot, node, n, ms);
 #pragma unroll
-      for (int c = 0; c < 9; ++c) js[c * tot + t] = m[(1 + c) * ms];
+        for (int c = 0; c < 9; ++c) js[c * tot + t] = m[(1 + c) * ms];
+      }
     }
   }
   __syncthreads();
@@ -184,43 +198,92 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
       double acc[NG];
 #pragma unroll
       for (int c = 0; c < NG; ++c) acc[c] = 0.0;
-      // xi direction
-      {
-        const double wo = T.w[1][j] * T.w[2][k];
-        for (int m = 0; m < n1p; ++m) {
-          const int idx = eb + m + n1p * (j + n2p * k);
-          const double dw = T.dh[0][m * 8 + i] * wo;
+      if (aff) {
+        // reference-space weak derivatives of g, then the constant metric transform
+        double W[3][NGV];
 #pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const double ja = js[(0 * 3 + d) * tot + idx] * dw;
+        for (int c = 0; c < 3 * NGV; ++c) W[c / NGV][c % NGV] = 0.0;
+        {
+          const double wo = T.w[1][j] * T.w[2][k];
 #pragma unroll
-            for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+          for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+            if (NX < 0 && m >= n1p) break;
+            const int idx = eb + m + n1p * (j + n2p * k);
+            const double dw = T.dh[0][m * 8 + i] * wo;
+#pragma unroll
+            for (int kk = 0; kk < NGV; ++kk) W[0][kk] += dw * gs[kk * tot + idx];
           }
         }
-      }
-      {
-        const double wo = T.w[0][i] * T.w[2][k];
-        for (int m = 0; m < n2p; ++m) {
-          const int idx = eb + i + n1p * (m + n2p * k);
-          const double dw = T.dh[1][m * 8 + j] * wo;
+        {
+          const double wo = T.w[0][i] * T.w[2][k];
 #pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const double ja = js[(1 * 3 + d) * tot + idx] * dw;
+          for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+            if (NX < 0 && m >= n2p) break;
+            const int idx = eb + i + n1p * (m + n2p * k);
+            const double dw = T.dh[1][m * 8 + j] * wo;
 #pragma unroll
-            for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+            for (int kk = 0; kk < NGV; ++kk) W[1][kk] += dw * gs[kk * tot + idx];
           }
         }
-      }
-      {
-        const double wo = T.w[0][i] * T.w[1][j];
-        for (int m = 0; m < n3p; ++m) {
-          const int idx = eb + i + n1p * (j + n2p * m);
-          const double dw = T.dh[2][m * 8 + k] * wo;
+        {
+          const double wo = T.w[0][i] * T.w[1][j];
+#pragma unroll
+          for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+            if (NX < 0 && m >= n3p) break;
+            const int idx = eb + i + n1p * (j + n2p * m);
+            const double dw = T.dh[2][m * 8 + k] * wo;
+#pragma unroll
+            for (int kk = 0; kk < NGV; ++kk) W[2][kk] += dw * gs[kk * tot + idx];
+          }
+        }
+        const double* mj = P.metrics + P.metric_off[slot] + 1;   // Ja^i_d at [3 i + d]
+#pragma unroll
+        for (int ii = 0; ii < 3; ++ii) {
 #pragma unroll
           for (int d = 0; d < 3; ++d) {
-            const double ja = js[(2 * 3 + d) * tot + idx] * dw;
+            const double ja = mj[3 * ii + d];
 #pragma unroll
-            for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+            for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * W[ii][kk];
+          }
+        }
+      } else {
+        {
+          const double wo = T.w[1][j] * T.w[2][k];
+          for (int m = 0; m < n1p; ++m) {
+            const int idx = eb + m + n1p * (j + n2p * k);
+            const double dw = T.dh[0][m * 8 + i] * wo;
+  #pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const double ja = js[(0 * 3 + d) * tot + idx] * dw;
+  #pragma unroll
+              for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+            }
+          }
+        }
+        {
+          const double wo = T.w[0][i] * T.w[2][k];
+          for (int m = 0; m < n2p; ++m) {
+            const int idx = eb + i + n1p * (m + n2p * k);
+            const double dw = T.dh[1][m * 8 + j] * wo;
+  #pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const double ja = js[(1 * 3 + d) * tot + idx] * dw;
+  #pragma unroll
+              for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+            }
+          }
+        }
+        {
+          const double wo = T.w[0][i] * T.w[1][j];
+          for (int m = 0; m < n3p; ++m) {
+            const int idx = eb + i + n1p * (j + n2p * m);
+            const double dw = T.dh[2][m * 8 + k] * wo;
+  #pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const double ja = js[(2 * 3 + d) * tot + idx] * dw;
+  #pragma unroll
+              for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+            }
           }
         }
       }
@@ -292,7 +355,7 @@ struct FluxArgs {
   int* nonfinite;
 };
 
-template <int LAW, int MODE>
+template <int LAW, int MODE, int NX>
 __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
@@ -300,7 +363,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   extern __shared__ double sm[];
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.orders + 3 * wi.x;
-  const int N1 = od[0], N2 = od[1], N3 = od[2];
+  const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
   load_tables(P, N1, N2, N3, T);
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
@@ -353,7 +416,9 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
       for (int v = 0; v < NV; ++v) F[v] = 0.0;
       {
         const double wo = T.w[1][j] * T.w[2][k];
-        for (int m = 0; m < n1p; ++m) {
+#pragma unroll
+        for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+          if (NX < 0 && m >= n1p) break;
           const int idx = eb + m + n1p * (j + n2p * k);
           const double dw = T.dh[0][m * 8 + i] * wo;
 #pragma unroll
@@ -362,7 +427,9 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
       }
       {
         const double wo = T.w[0][i] * T.w[2][k];
-        for (int m = 0; m < n2p; ++m) {
+#pragma unroll
+        for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+          if (NX < 0 && m >= n2p) break;
           const int idx = eb + i + n1p * (m + n2p * k);
           const double dw = T.dh[1][m * 8 + j] * wo;
 #pragma unroll
@@ -371,7 +438,9 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
       }
       {
         const double wo = T.w[0][i] * T.w[1][j];
-        for (int m = 0; m < n3p; ++m) {
+#pragma unroll
+        for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+          if (NX < 0 && m >= n3p) break;
           const int idx = eb + i + n1p * (j + n2p * m);
           const double dw = T.dh[2][m * 8 + k] * wo;
 #pragma unroll
