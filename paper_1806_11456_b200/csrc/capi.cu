@@ -9,6 +9,7 @@
 #include <type_traits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -20,6 +21,7 @@
 #include "laws.cuh"
 #include "transfer.cuh"
 #include "volume.cuh"
+#include "volume_tma.cuh"
 
 using namespace tdg;
 
@@ -135,6 +137,9 @@ struct tdg_plan {
   size_t smem_lift = 0, smem_flux = 0;
   int64_t side_nodes = 0;
   int iso = -1;          // isotropic order of a single-bucket plan, else -1
+  bool tma = false;      // persistent TMA-pipelined flux kernel (TDG_TMA=1 enables)
+  int nsm = 148;
+  size_t smem_flux_tma = 0;
 };
 
 struct tdg_transfer {
@@ -187,6 +192,12 @@ int setup_attrs(tdg_plan* p) {
     if ((rc = allow_smem(k_vol_flux<LAW, MODE_R, NX>, p->smem_flux))) return rc;
     if ((rc = allow_smem(k_vol_flux<LAW, MODE_RK, NX>, p->smem_flux))) return rc;
     if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, NX>, p->smem_flux))) return rc;
+    const size_t tb = p->smem_flux_tma;
+    if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_F, NX>, tb))) return rc;
+    if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_A, NX>, tb))) return rc;
+    if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_R, NX>, tb))) return rc;
+    if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_RK, NX>, tb))) return rc;
+    if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_TAU, NX>, tb))) return rc;
     return TDG_OK;
   });
 }
@@ -254,7 +265,13 @@ int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cuda
   {
     KTimer kt(TDG_K_VOL_FLUX, st);
     with_nx<LAW>(p->iso, [&](auto nx) -> int {
-      k_vol_flux<LAW, MODE, decltype(nx)::value><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a);
+      constexpr int NX = decltype(nx)::value;
+      if (p->tma) {
+        const int grid = std::min(p->d.nwork, p->nsm);
+        k_vol_flux_tma<LAW, MODE, NX><<<grid, TMA_THREADS, p->smem_flux_tma, st>>>(p->d, Q, a);
+      } else {
+        k_vol_flux<LAW, MODE, NX><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a);
+      }
       return 0;
     });
   }
@@ -472,6 +489,18 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.grad = grad;
   p->smem_lift = static_cast<size_t>(std::max(p->ngv + 9, NG)) * MAXN * sizeof(double);
   p->smem_flux = static_cast<size_t>(3 * p->nv) * MAXN * sizeof(double);
+  p->smem_flux_tma = static_cast<size_t>(p->nv == 5 ? tma_flux_smem_doubles<5, 12>()
+                                                    : tma_flux_smem_doubles<1, 3>()) * sizeof(double);
+  {
+    // measured slower than the 3-blocks/SM kernel at one block per SM
+    // (compute-phase latency dominates once loads are decoupled); opt-in
+    const char* env = getenv("TDG_TMA");
+    p->tma = env && env[0] == '1';
+    int dev = 0, nsm = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
+      p->nsm = nsm;
+  }
   switch (d.law) {
     case TDG_LAW_ADVDIFF: rc = setup_attrs<LAW_ADVDIFF>(p); break;
     case TDG_LAW_BURGERS: rc = setup_attrs<LAW_BURGERS>(p); break;

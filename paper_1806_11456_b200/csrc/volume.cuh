@@ -411,9 +411,12 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
       const int e = t / n, node = t - e * n, slot = wi.x + e;
       const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
       const int eb = e * n;
-      double F[NV];
+      double F[NV], F0[NV], F1[NV], F2[NV];   // per-direction chains (ILP)
 #pragma unroll
-      for (int v = 0; v < NV; ++v) F[v] = 0.0;
+      for (int v = 0; v < NV; ++v) {
+        F[v] = 0.0;
+        F0[v] = F1[v] = F2[v] = 0.0;
+      }
       {
         const double wo = T.w[1][j] * T.w[2][k];
 #pragma unroll
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
           const int idx = eb + m + n1p * (j + n2p * k);
           const double dw = T.dh[0][m * 8 + i] * wo;
 #pragma unroll
-          for (int v = 0; v < NV; ++v) F[v] -= dw * ft[(0 * NV + v) * tot + idx];
+          for (int v = 0; v < NV; ++v) F0[v] += dw * ft[(0 * NV + v) * tot + idx];
         }
       }
       {
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
           const int idx = eb + i + n1p * (m + n2p * k);
           const double dw = T.dh[1][m * 8 + j] * wo;
 #pragma unroll
-          for (int v = 0; v < NV; ++v) F[v] -= dw * ft[(1 * NV + v) * tot + idx];
+          for (int v = 0; v < NV; ++v) F1[v] += dw * ft[(1 * NV + v) * tot + idx];
         }
       }
       {
@@ -444,9 +447,11 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
           const int idx = eb + i + n1p * (j + n2p * m);
           const double dw = T.dh[2][m * 8 + k] * wo;
 #pragma unroll
-          for (int v = 0; v < NV; ++v) F[v] -= dw * ft[(2 * NV + v) * tot + idx];
+          for (int v = 0; v < NV; ++v) F2[v] += dw * ft[(2 * NV + v) * tot + idx];
         }
       }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) F[v] -= (F0[v] + F1[v]) + F2[v];
       const int ijk[3] = {i, j, k};
       const int np[3] = {n1p, n2p, n3p};
 #pragma unroll
