@@ -40,14 +40,15 @@ def select_orders(tmap, cfg):
     lo, hi = cfg.n_min, cfg.n_max
     for e in range(nel):
         p = tmap.fine_orders.orders[e]
-        act = [d for d in range(3) if p[d] > 0]
+        frozen = getattr(tmap, "frozen", set())
+        act = [d for d in range(3) if p[d] > 0 and d not in frozen]
         for d in act:
             if not tmap.tau[e][d]:
                 raise AdaptationError(f"element {e} has an empty truncation-error map")
 
         def combos(choices):
             for vals in itertools.product(*choices):
-                n = [0, 0, 0]
+                n = [int(x) for x in p]                 # frozen directions keep their order
                 for d, v in zip(act, vals):
                     n[d] = v
                 yield tuple(n)
@@ -69,7 +70,7 @@ def select_orders(tmap, cfg):
         if feasible:
             n, v = min(feasible, key=lambda it: _key(it[0]))
         else:
-            n = tuple(hi if d in act else 0 for d in range(3))
+            n = tuple(hi if d in act else int(p[d]) for d in range(3))
             v = tmap.combined(e, n)
             v = float("inf") if v is None else v
             path = "fallback-N_max"

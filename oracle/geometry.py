@@ -62,8 +62,10 @@ def volume_metrics(ctrl, orders, family="LG", form="cross", index=-1):
     """Returns (jac (n1,n2,n3), ja (3, 3, n1,n2,n3) with ja[i, n] = Ja^i_n,
     sizes (3,))."""
     m = [s - 1 for s in ctrl.shape[:3]]
+    # the cross-product form needs a sub/isoparametric map (reference
+    # mesh.py:147-152); the curl form works with I^N of the map by design
     for d in range(3):
-        if orders[d] >= 1 and m[d] > orders[d]:
+        if form == "cross" and orders[d] >= 1 and m[d] > orders[d]:
             raise MeshError(
                 f"element {index}: mapping order {tuple(m)} exceeds solution order {tuple(orders)}"
             )

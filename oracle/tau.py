@@ -42,6 +42,9 @@ class TauMap:
         self.non_spectral = [[False, False, False] for _ in range(n)]
         self.n_max = fine_orders.max_order()
         self.work_units = 0.0
+        # directions held at their fine order (never estimated / adapted):
+        # collapsed order-0 directions plus any the caller freezes
+        self.frozen = {d for d in range(3) if int(np.max(fine_orders.orders[:, d])) == 0}
 
     @property
     def num_elements(self):
@@ -59,8 +62,8 @@ class TauMap:
     def combined(self, e, n):
         total = 0.0
         for d in range(3):
-            if self.fine_orders.orders[e, d] == 0 and n[d] == 0 and not self.tau[e][d]:
-                continue                      # collapsed direction: no contribution
+            if d in self.frozen:
+                continue                      # collapsed / frozen direction: no contribution
             t = self.tau[e][d].get(int(n[d]))
             if t is None:
                 return None
@@ -86,7 +89,7 @@ def recorder_for(tmap, direction):
     return recorder
 
 
-def estimate(msh, law, Q, tau_max, isolated=True, fine_op=None, family="LG", form="cross"):
+def estimate(msh, law, Q, tau_max, isolated=True, fine_op=None, family="LG", form="cross", frozen=()):
     """tau.py:188-224: convergence gate, then one smoothing-free anisotropic
     high-order descent per direction."""
     from .operators import DGOperator
@@ -99,9 +102,10 @@ def estimate(msh, law, Q, tau_max, isolated=True, fine_op=None, family="LG", for
         raise EstimationError(f"insufficient convergence for estimation: |r|={rnorm:.3e} "
                               f"exceeds tau_max/10={threshold:.3e}")
     tmap = TauMap(orders, EstimationContext(threshold, rnorm, isolated))
+    tmap.frozen |= set(frozen)
     tmap.work_units = 1.0 / 3.0
     for direction in (1, 2, 3):
-        if orders.max_order_dir(direction) <= multigrid.N_COARSE:
+        if orders.max_order_dir(direction) <= multigrid.N_COARSE or direction - 1 in tmap.frozen:
             continue
         solver = multigrid.FASSolver(msh, law, orders, rule="high-order", direction=direction,
                                      fine_op=op, family=family, form=form)
@@ -124,7 +128,7 @@ def extrapolate_map(tmap, n_max):
     for e in range(tmap.num_elements):
         for d in range(3):
             p = int(tmap.fine_orders.orders[e, d])
-            if p == 0:
+            if p == 0 or d in tmap.frozen:
                 continue                      # collapsed direction
             points = [(n, v) for n, v in tmap.tau[e][d].items()
                       if n not in tmap.extrapolated[e][d] and v > 0.0]

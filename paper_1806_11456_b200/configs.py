@@ -27,7 +27,23 @@ class Workload:
     family: str = "LGL"
     form: str = "curl"
     smoother: dict = field(default_factory=dict)
+    time: dict = field(default_factory=dict)     # TimeConfig kwargs (CFL constants)
     notes: str = ""
+
+
+def hashed_noise(seed, amp):
+    """Deterministic per-point noise in [-amp, amp) from the node position
+    (a seeded hash), so CPU oracle and GPU get bit-identical inputs whatever
+    order they evaluate nodes in."""
+    rng = np.random.default_rng(seed)
+    a = rng.uniform(10.0, 100.0, 3)
+    ph = rng.uniform(0.0, 1.0, 5)
+
+    def fn(x, y, z, comp):
+        s = np.sin(a[0] * x + a[1] * y + a[2] * z + 7.0 * comp + ph[comp]) * 43758.5453123
+        return amp * (2.0 * (s - np.floor(s)) - 1.0)
+
+    return fn
 
 
 def sinusoid_perturbation(law, rng, amp, kz=True, terms=4, kmax=3, box=(1.0, 1.0, 1.0)):
@@ -78,8 +94,7 @@ def config4(seed=4, n=24, order=7) -> Workload:
     L = 2.0 * np.pi
     msh = mesh.build_box(n, n, n, bounds=((0, L), (0, L), (0, L)))
     law = physics.NavierStokes(gamma=1.4, prandtl=0.72, mach=0.1, reynolds=1600.0)
-    rng = np.random.default_rng(seed)
-    noise_cache = {}
+    noise = hashed_noise(seed, 1e-3)
     p0 = 1.0 / (law.gamma * law.mach ** 2)
 
     def init(x, y, z):
@@ -88,14 +103,73 @@ def config4(seed=4, n=24, order=7) -> Workload:
         w = 0.0 * x
         p = p0 + (np.cos(2 * x) + np.cos(2 * y)) * (np.cos(2 * z) + 2.0) / 16.0
         q = law.conservative(1.0 + 0.0 * x, u, v, w, p)
-        key = q.shape
-        if key not in noise_cache:
-            noise_cache[key] = rng.uniform(-1e-3, 1e-3, q.shape)
-        return q + noise_cache[key]
+        return q + np.stack([noise(x, y, z, c) for c in range(5)])
 
     return Workload(f"cfg4: {n}^3 periodic affine (2pi), N={order} LGL, TGV M=0.1 Re=1600", msh, law,
                     OrderField.uniform(n ** 3, order), init,
                     smoother=dict(pre_sweeps=2, post_sweeps=2, coarsest_sweeps=2, max_batches=1))
 
 
-CONFIGS = {1: config1, 3: config3, 4: config4}
+def config2(seed=1, nx=40, ny=20, order=5, dz=0.05, nz_order=1) -> Workload:
+    """Flat-plate-type steady case: x in [-0.5, 1], y in [0, 0.5], one element
+    deep (dz, self-periodic, Nz held at 1), 40 x 20 elements graded (ratio 1.1)
+    toward y = 0 and, two-sided, toward x = 0 (13 cells on the x < 0 side, 27
+    on x >= 0).  No-slip adiabatic wall for x >= 0 and symmetry for x < 0 at
+    y = 0, freestream elsewhere; M = 0.2, Re = 1e5 per unit length; freestream
+    plus 1e-3 seeded nodal noise (relative to |q_inf| per variable)."""
+    nl = int(round(nx * 0.5 / 1.5))
+    xl = mesh.grade_coordinates(nl, -0.5, 0.0, 1.1, at_start=False)
+    xr = mesh.grade_coordinates(nx - nl, 0.0, 1.0, 1.1, at_start=True)
+    xs = np.concatenate([xl, xr[1:]])
+    ys = mesh.grade_coordinates(ny, 0.0, 0.5, 1.1, at_start=True)
+    zs = np.array([0.0, dz])
+    msh = mesh.build_box(nx, ny, 1, coords=(xs, ys, zs), periodic=(False, False, True))
+    # split the y = 0 boundary: wall for x >= 0, symmetry for x < 0
+    faces = msh.faces
+    tags = {}
+    for fi, f in enumerate(faces):
+        if f.is_boundary:
+            if f.tag == "south":
+                xc = msh.nodes[f.left][..., 0].mean()
+                f.tag = "wall" if xc >= 0.0 else "symmetry"
+            tags.setdefault(f.tag, []).append(fi)
+    msh.boundary_tags = tags
+    msh.bc = {"wall": "wall", "symmetry": "symmetry", "west": "freestream", "east": "freestream",
+              "north": "freestream"}
+    law = physics.NavierStokes(gamma=1.4, prandtl=0.72, mach=0.2, reynolds=1e5)
+    fs = law.freestream()
+    noise = hashed_noise(seed, 1e-3)
+
+    def init(x, y, z):
+        return np.stack([fs[c] + 0.0 * x + noise(x, y, z, c) * max(abs(fs[c]), 1.0) for c in range(5)])
+
+    orders = np.tile([order, order, nz_order], (nx * ny, 1))
+    return Workload(f"cfg2: {nx}x{ny}x1 graded flat plate, N={order} (Nz={nz_order}) LGL, NS M=0.2 Re=1e5",
+                    msh, law, OrderField(orders), init,
+                    smoother=dict(pre_sweeps=3, post_sweeps=3, coarsest_sweeps=10, max_batches=1),
+                    notes="Nz held at 1 (not adapted); two-sided x clustering 13/27 cells")
+
+
+def config5(seed=5, na=16, nr=24, order=3, r1=10.0) -> Workload:
+    """Cubed-sphere shell r in [0.5, 10] around a unit-diameter sphere, 6 blocks
+    of na x na x nr elements, radial ratio 1.15, geometry at the solution
+    order; no-slip adiabatic wall on the sphere, freestream outside; M = 0.2,
+    Re = 200; freestream plus 1e-3 seeded noise."""
+    msh = mesh.build_cubed_sphere(na, nr, 0.5, r1, 1.15, mapping_order=order)
+    law = physics.NavierStokes(gamma=1.4, prandtl=0.72, mach=0.2, reynolds=200.0)
+    fs = law.freestream()
+    noise = hashed_noise(seed, 1e-3)
+
+    def init(x, y, z):
+        return np.stack([fs[c] + 0.0 * x + noise(x, y, z, c) * max(abs(fs[c]), 1.0) for c in range(5)])
+
+    nel = msh.num_elements
+    return Workload(f"cfg5: cubed-sphere shell 6x{na}x{na}x{nr}, N={order} LGL curved, NS M=0.2 Re=200",
+                    msh, law, OrderField.uniform(nel, order), init,
+                    smoother=dict(pre_sweeps=3, post_sweeps=3, coarsest_sweeps=5, max_batches=1),
+                    time=dict(cfl_advective=0.05, cfl_viscous=0.025),
+                    notes="CFL 0.05/0.025: the max(N,1)^2 bound under-estimates N=1 stiffness on "
+                          "curved shell elements (SURVEY §0.7)")
+
+
+CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}

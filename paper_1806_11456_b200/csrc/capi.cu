@@ -182,24 +182,26 @@ int with_nx(int iso, F&& f) {
 
 template <int LAW>
 int setup_attrs(tdg_plan* p) {
-  using L = Law<LAW>;
-  return with_nx<LAW>(p->iso, [&](auto nx) -> int {
+  int rc = with_nx<LAW>(p->iso, [&](auto nx) -> int {
     constexpr int NX = decltype(nx)::value;
-    int rc;
-    if ((rc = allow_smem(k_vol_lift<LAW, NX>, p->smem_lift))) return rc;
-    if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, NX>, p->smem_flux))) return rc;
-    if ((rc = allow_smem(k_vol_flux<LAW, MODE_A, NX>, p->smem_flux))) return rc;
-    if ((rc = allow_smem(k_vol_flux<LAW, MODE_R, NX>, p->smem_flux))) return rc;
-    if ((rc = allow_smem(k_vol_flux<LAW, MODE_RK, NX>, p->smem_flux))) return rc;
-    if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, NX>, p->smem_flux))) return rc;
-    const size_t tb = p->smem_flux_tma;
-    if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_F, NX>, tb))) return rc;
-    if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_A, NX>, tb))) return rc;
-    if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_R, NX>, tb))) return rc;
-    if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_RK, NX>, tb))) return rc;
-    if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_TAU, NX>, tb))) return rc;
+    int r;
+    if ((r = allow_smem(k_vol_lift<LAW, NX>, p->smem_lift))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX>, p->smem_flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX>, p->smem_flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX>, p->smem_flux))) return r;
     return TDG_OK;
   });
+  if (rc) return rc;
+  // cold modes and the opt-in TMA kernel use runtime orders only
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, -1>, p->smem_flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, -1>, p->smem_flux))) return rc;
+  const size_t tb = p->smem_flux_tma;
+  if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_F, -1>, tb))) return rc;
+  if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_A, -1>, tb))) return rc;
+  if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_R, -1>, tb))) return rc;
+  if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_RK, -1>, tb))) return rc;
+  if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_TAU, -1>, tb))) return rc;
+  return TDG_OK;
 }
 
 // trace -> lift (if viscous) -> face fluxes; leaves fsurf ready for k_vol_flux
@@ -264,16 +266,18 @@ int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cuda
   if (p->d.nwork == 0) return TDG_OK;
   {
     KTimer kt(TDG_K_VOL_FLUX, st);
-    with_nx<LAW>(p->iso, [&](auto nx) -> int {
-      constexpr int NX = decltype(nx)::value;
-      if (p->tma) {
-        const int grid = std::min(p->d.nwork, p->nsm);
-        k_vol_flux_tma<LAW, MODE, NX><<<grid, TMA_THREADS, p->smem_flux_tma, st>>>(p->d, Q, a);
-      } else {
-        k_vol_flux<LAW, MODE, NX><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a);
-      }
-      return 0;
-    });
+    constexpr bool hot = MODE == MODE_R || MODE == MODE_RK || MODE == MODE_A;
+    if (p->tma) {
+      const int grid = std::min(p->d.nwork, p->nsm);
+      k_vol_flux_tma<LAW, MODE, -1><<<grid, TMA_THREADS, p->smem_flux_tma, st>>>(p->d, Q, a);
+    } else if (hot) {
+      with_nx<LAW>(p->iso, [&](auto nx) -> int {
+        k_vol_flux<LAW, MODE, hot ? decltype(nx)::value : -1><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a);
+        return 0;
+      });
+    } else {
+      k_vol_flux<LAW, MODE, -1><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a);
+    }
   }
   LAUNCH_CHECK("k_vol_flux");
   return TDG_OK;

@@ -58,8 +58,10 @@ def _coll(arr, axis, D):
 def volume_metrics(nodes, orders, family, form, ids=None):
     """Returns J (B,n1,n2,n3), Ja (B,3,3,n1,n2,n3) [i, phys], sizes (B,3), coords."""
     m = [s - 1 for s in nodes.shape[1:4]]
+    # cross form: sub/isoparametric only (reference mesh.py:147-152); the
+    # invariant curl form uses the interpolant I^N of the map (PAPER.md:144-149)
     for d in range(3):
-        if orders[d] >= 1 and m[d] > orders[d]:
+        if form == "cross" and orders[d] >= 1 and m[d] > orders[d]:
             raise MeshError(f"mapping order {tuple(m)} exceeds solution order {tuple(orders)}")
     x = [spectral.rule(int(n), family)[0] for n in orders]
     w = [spectral.rule(int(n), family)[1] for n in orders]

@@ -433,3 +433,84 @@ def build_rotated_box(nx: int, ny: int, nz: int, bounds=((0.0, 1.0), (0.0, 1.0),
     nodes = trilinear_nodes(corners)
     faces, tags = faces_from_hexes(hexes, lambda e, s: "boundary")
     return HexMesh(nodes, faces, tags, dict(bc or {}))
+
+
+def _cube_face_dirs():
+    """Six cube faces as (normal axis, sign, tangent axes): equiangular blocks."""
+    return [(0, +1), (0, -1), (1, +1), (1, -1), (2, +1), (2, -1)]
+
+
+def build_cubed_sphere(na: int, nr: int, r0: float = 0.5, r1: float = 10.0, ratio: float = 1.15,
+                       mapping_order: int = 3, bc=None) -> HexMesh:
+    """Equiangular cubed-sphere shell: 6 blocks of na x na (angular) x nr
+    (radial) elements between radii r0 and r1, radial sizes growing
+    geometrically by ``ratio`` away from the inner sphere.  Geometry is the
+    analytic map sampled on an equispaced control grid of ``mapping_order``
+    per direction (curved elements).  Connectivity comes from vertex matching
+    across block seams, so seam faces carry general orientation codes.
+    Boundary tags: 'wall' (inner sphere), 'freestream' (outer)."""
+    rs = grade_coordinates(nr, r0, r1, ratio, at_start=True)
+    ang = np.linspace(-np.pi / 4, np.pi / 4, na + 1)
+    m = mapping_order
+
+    def direction(axis, sign, a, b):
+        ta, tb = np.tan(a), np.tan(b)
+        v = [None, None, None]
+        others = [x for x in range(3) if x != axis]
+        v[axis] = sign * np.ones_like(ta)
+        v[others[0]] = ta
+        v[others[1]] = tb
+        v = np.stack(v, axis=-1)
+        return v / np.linalg.norm(v, axis=-1, keepdims=True)
+
+    def point(axis, sign, a, b, r):
+        return direction(axis, sign, a, b) * np.asarray(r)[..., None]
+
+    # vertex lattice per block, merged across seams by rounded coordinates
+    all_pts, blocks = [], []
+    for axis, sign in _cube_face_dirs():
+        A, B, R = np.meshgrid(ang, ang, rs, indexing="ij")
+        P = point(axis, sign, A, B, R)
+        blocks.append((axis, sign))
+        all_pts.append(P.reshape(-1, 3))
+    pts = np.concatenate(all_pts)
+    _, inverse = np.unique(np.round(pts, 10), axis=0, return_inverse=True)
+    vid = inverse.reshape(6, na + 1, na + 1, nr + 1)
+    nel = 6 * na * na * nr
+    hexes = np.empty((nel, 2, 2, 2), dtype=np.int64)
+    nodes = np.empty((nel, m + 1, m + 1, m + 1, 3))
+    g = np.linspace(0.0, 1.0, m + 1)
+    e = 0
+    for bi, (axis, sign) in enumerate(blocks):
+        for k in range(nr):
+            for j in range(na):
+                for i in range(na):
+                    # local (a, b, r); flip a for negatively oriented blocks
+                    a0, a1 = ang[i], ang[i + 1]
+                    b0, b1 = ang[j], ang[j + 1]
+                    rr0, rr1 = rs[k], rs[k + 1]
+                    A = a0 + (a1 - a0) * g[:, None, None]
+                    B = b0 + (b1 - b0) * g[None, :, None]
+                    Rr = rr0 + (rr1 - rr0) * g[None, None, :]
+                    A, B, Rr = np.broadcast_arrays(A, B, Rr)
+                    X = point(axis, sign, A, B, Rr)
+                    ids = vid[bi, i:i + 2, j:j + 2, k:k + 2]
+                    # orientation: make the local frame right-handed
+                    a1v = X[-1, 0, 0] - X[0, 0, 0]
+                    b1v = X[0, -1, 0] - X[0, 0, 0]
+                    r1v = X[0, 0, -1] - X[0, 0, 0]
+                    if np.dot(np.cross(a1v, b1v), r1v) < 0:
+                        X = X[::-1]
+                        ids = ids[::-1]
+                    nodes[e] = X
+                    hexes[e] = ids
+                    e += 1
+
+    def tag(el, side):
+        # radial direction is local zeta: bottom = inner sphere, top = outer
+        return "wall" if side == BOTTOM else "freestream"
+
+    faces, tags = faces_from_hexes(hexes, tag)
+    bcs = {"wall": "wall", "freestream": "freestream"}
+    bcs.update(bc or {})
+    return HexMesh(nodes, faces, tags, bcs)

@@ -215,6 +215,30 @@ def tau_case():
         save(f"tau_{name}", case=case, orders=of.orders, Q=flat(Q), **out, **mesh_arrays(m))
 
 
+ADAPT_CASES = {
+    "single_sine_p4": dict(stages=(4,), tau_max=1e-2, n_max=6, final_tol=1e-9),
+    "multi_sine_2_4": dict(stages=(2, 4), tau_max=1e-5, n_max=6, final_tol=1e-8),
+}
+
+
+def adapt_case(name, spec):
+    m = mesh.build_cartesian(2, 2)
+    law = physics.make_case("advdiff-sine")
+    cfg = ad.AdaptConfig(tau_max=spec["tau_max"], n_max=spec["n_max"], stages=spec["stages"])
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", RuntimeWarning)
+        run = ad.run_multi_stage(m, law, cfg, final_tol=spec["final_tol"])
+    out = {"final_orders": run.orders.orders, "Q": flat(run.Q), "work_units": run.work_units,
+           "nreports": len(run.reports), "stages": np.array(spec["stages"]), "tau_max": spec["tau_max"],
+           "n_max": spec["n_max"], "final_tol": spec["final_tol"]}
+    for i, rep in enumerate(run.reports):
+        out[f"rep{i}_new"] = np.array([d.new_orders for d in rep.decisions])
+        out[f"rep{i}_paths"] = np.array([d.path for d in rep.decisions])
+        out[f"rep{i}_pred"] = np.array([d.predicted_tau for d in rep.decisions])
+        out[f"rep{i}_dofs"] = np.array([rep.dofs_before, rep.dofs_after])
+    save(f"adapt_{name}", case="advdiff-sine", **out, **mesh_arrays(m))
+
+
 def main():
     np.set_printoptions(precision=3)
     spectral_case()
@@ -224,6 +248,8 @@ def main():
     for name, spec in MG_CASES.items():
         mg_case(name, spec)
     tau_case()
+    for name, spec in ADAPT_CASES.items():
+        adapt_case(name, spec)
 
 
 if __name__ == "__main__":
