@@ -332,6 +332,33 @@ def run_b200(args):
                   "rnorm_post": [float(x) for x in hist[-len(times):]]}
         del solver
 
+    # small configs: V-cycle latency (CUDA-graph replay of pinned-sweep cycles)
+    small = {}
+    if not args.no_vcycle:
+        import warnings
+
+        from paper_1806_11456_b200 import timestep
+
+        for cid in (1, 2):
+            wk = configs.CONFIGS[cid]()
+            sv = multigrid.FASSolver(wk.mesh, wk.law, wk.orders, smoother=multigrid.SmootherConfig(**wk.smoother),
+                                     time_config=timestep.TimeConfig(**wk.time), family=wk.family, form=wk.form)
+            sv.set_state(sv.finest.op.project_function(wk.init))
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", RuntimeWarning)
+                sv.v_cycle()
+                torch.cuda.synchronize()
+                a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(5):
+                    sv.v_cycle()
+                b2.record(stream)
+                torch.cuda.synchronize()
+            small[f"cfg{cid}_vcycle_ms"] = max_over_ranks(a.elapsed_time(b2) / 5)
+            del sv
+        if vcycle is not None:
+            vcycle.update(small)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, info = cpu_sample_rate(n=6, budget_s=args.cpu_budget)

@@ -102,6 +102,10 @@ struct KTimer {
   TimedLaunch t;
   cudaStream_t st;
   KTimer(int kind, cudaStream_t s) : on(g_timing), st(s) {
+    if (on) {  // never record timing events into a CUDA-graph capture
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) on = false;
+    }
     if (!on) return;
     t.kind = kind;
     t.a = take_event();
@@ -428,12 +432,22 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
         if (p->orders_h[3 * s + dd] != iso) iso = -1;
     p->iso = iso;
   }
-  // element work items: runs of identical orders, <= MAXN nodes
+  // element work items: runs of identical orders, <= MAXN nodes; small
+  // plans get smaller items so that every SM receives work (>= 2 per SM)
+  int nsm_attr = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&nsm_attr, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      nsm_attr = 148;
+  }
+  const long long item_nodes =
+      std::max<long long>(1, std::min<long long>(MAXN, p->nodes / (2LL * nsm_attr)));
   std::vector<int2> work;
   for (int s = 0; s < ns;) {
     const int* o = &p->orders_h[3 * s];
     const int n = (o[0] + 1) * (o[1] + 1) * (o[2] + 1);
-    const int cap = std::max(1, MAXN / n);
+    const int cap = std::max(1, static_cast<int>(item_nodes / n));
     int e = s;
     while (e < ns && e - s < cap && p->orders_h[3 * e] == o[0] && p->orders_h[3 * e + 1] == o[1] &&
            p->orders_h[3 * e + 2] == o[2])
