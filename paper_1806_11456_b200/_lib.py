@@ -11,7 +11,8 @@ import os
 from .errors import ConfigError, DeviceError, MeshError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_taudg.so")
+# TDG_LIB_PATH: development override (A/B builds of the same C-ABI)
+LIB_PATH = os.environ.get("TDG_LIB_PATH") or os.path.join(_HERE, "_taudg.so")
 
 _i32, _i64, _dbl = C.c_int32, C.c_int64, C.c_double
 _pd, _pi32, _pi64 = C.POINTER(C.c_double), C.POINTER(C.c_int32), C.POINTER(C.c_int64)

@@ -122,60 +122,57 @@ __device__ __forceinline__ void block_max_to(double v, double* out, double* red 
   __syncthreads();
 }
 
-// One warp projects C component arrays of (na x nb) values (a fastest) to
-// (ma x mb):  dst[c][A + ma B] = sum_{a,b} T1[A][a] T2[B][b] src[c][a + na b]
-// (T rows stride 8).  All components are staged together (coalesced loads),
-// then two separable passes; three __syncwarp per call.  s_in/s_tmp hold
-// C*64 doubles each.
+// FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col); per lane
+// a = A[lane/4][lane%4], b = B[lane%4][lane/4], d = D[lane/4][2(lane%4) + {0,1}].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// One warp projects C component arrays of (na x nb) values to (ma x mb):
+//   out[c][A, B] = sum_b T2[B][b] sum_a T1[A][a] in[c][a, b]      (T rows stride 8)
+// on the FP64 tensor cores, one zero-padded 8x8 tile per component and pass:
+// pass 1 (M = A, K = a, N = b) takes its B operand straight from ld(c, a, b);
+// its result stays in registers and reaches pass 2 (M = B, K = b, N = A)
+// through quad shuffles.  No shared memory, no __syncwarp; the whole warp
+// must be converged.  st(c, A, B, value) receives each output once.
 template <int C, class Load, class Store>
-__device__ __forceinline__ void warp_projC(int na, int nb, const double* __restrict__ T1, int ma,
-                                           const double* __restrict__ T2, int mb, double* s_in,
-                                           double* s_tmp, Load ld, Store st) {
+__device__ __forceinline__ void warp_proj_mma(int na, int nb, const double* __restrict__ T1, int ma,
+                                              const double* __restrict__ T2, int mb, Load ld,
+                                              Store st) {
   const int lane = threadIdx.x & 31;
-  // stage: lanes own input positions, loop over components (coalesced per c)
-  const int nin = na * nb;
-  for (int k = lane; k < nin; k += 32) {
+  const int g = lane >> 2, q = lane & 3;
+  const double t10 = (g < ma && q < na) ? T1[g * 8 + q] : 0.0;
+  const double t11 = (g < ma && q + 4 < na) ? T1[g * 8 + q + 4] : 0.0;
+  const double t20 = (g < mb && q < nb) ? T2[g * 8 + q] : 0.0;
+  const double t21 = (g < mb && q + 4 < nb) ? T2[g * 8 + q + 4] : 0.0;
+  const bool ka = na > 4, kb = nb > 4;
+  // pass-2 operand tmp[A = g][b = q (+4)] sits in lane (g, q/2 (+2)), element q&1
+  const int s0 = (g << 2) | (q >> 1), s1 = s0 + 2;
+  const bool odd = q & 1;
+  const bool colv = g < nb;
 #pragma unroll
-    for (int c = 0; c < C; ++c) s_in[c * 64 + k] = ld(c, k);
-  }
-  __syncwarp();
-  // pass 1 (along a): lanes own (A, b) positions; matrix row cached in registers
-  const int nt = ma * nb;
-  for (int k = lane; k < nt; k += 32) {
-    const int b = k / ma, A = k - b * ma;
-    double r[8];
-#pragma unroll
-    for (int a = 0; a < 8; ++a) r[a] = a < na ? T1[A * 8 + a] : 0.0;
-    const int base = na * b;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const double* col = s_in + c * 64 + base;
-      double acc = 0.0;
-#pragma unroll
-      for (int a = 0; a < 8; ++a)
-        if (a < na) acc += r[a] * col[a];
-      s_tmp[c * 64 + k] = acc;
+  for (int c = 0; c < C; ++c) {
+    double d0 = 0.0, d1 = 0.0;
+    const double b0 = (colv && q < na) ? ld(c, q, g) : 0.0;
+    const double b1 = (colv && ka && q + 4 < na) ? ld(c, q + 4, g) : 0.0;
+    dmma_8x8x4(d0, d1, t10, b0);
+    if (ka) dmma_8x8x4(d0, d1, t11, b1);
+    double o0 = 0.0, o1 = 0.0;
+    {
+      const double e0 = __shfl_sync(0xffffffffu, d0, s0), e1 = __shfl_sync(0xffffffffu, d1, s0);
+      dmma_8x8x4(o0, o1, t20, odd ? e1 : e0);
+    }
+    if (kb) {
+      const double e0 = __shfl_sync(0xffffffffu, d0, s1), e1 = __shfl_sync(0xffffffffu, d1, s1);
+      dmma_8x8x4(o0, o1, t21, odd ? e1 : e0);
+    }
+    if (g < mb) {
+      if (2 * q < ma) st(c, 2 * q, g, o0);
+      if (2 * q + 1 < ma) st(c, 2 * q + 1, g, o1);
     }
   }
-  __syncwarp();
-  // pass 2 (along b): lanes own (A, B) output positions
-  const int no = ma * mb;
-  for (int k = lane; k < no; k += 32) {
-    const int B = k / ma, A = k - B * ma;
-    double r[8];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) r[b] = b < nb ? T2[B * 8 + b] : 0.0;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const double* col = s_tmp + c * 64 + A;
-      double acc = 0.0;
-#pragma unroll
-      for (int b = 0; b < 8; ++b)
-        if (b < nb) acc += r[b] * col[ma * b];
-      st(c, k, acc);
-    }
-  }
-  __syncwarp();
 }
 
 // face coordinates of a side: normal direction and the two tangential ones

@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
   const bool conf = (L1 == M1) && (L2 == M2) && (R1 == M1) && (R2 == M2);
   const int A = t % (M1 + 1), B = t / (M1 + 1);
   const int kR = right_index(A, B, M1, M2, orient);
-  // conforming: own-order traces; nonconforming: mortar traces from k_up
+  // conforming: own-order traces; nonconforming: mortar traces (item_side_traces)
   const double* qsrc = conf ? P.qtr : P.qtrm;
   const double* gsrc = conf ? P.gtr : P.gtrm;
   const long long tL = conf ? P.side_off[slotL * 6 + sideL] : P.side_info[slotL * 6 + sideL].w;
@@ -105,40 +105,12 @@ __global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
   }
 }
 
-// Mortar interpolation of a nonconforming side's own-order traces (own frame):
-// one warp per side, all C components at once (warp_projC).
-template <int C>
-__global__ void __launch_bounds__(128) k_up(DevPlan P, const double* __restrict__ own,
-                                           double* __restrict__ mort) {
-  __shared__ double scr[4][2][C * 64];
-  const int warp = threadIdx.x >> 5;
-  const int task = blockIdx.x * 4 + warp;
-  if (task >= P.nup) return;
-  const int2 tk = P.up[task];
-  const int slot = tk.x, s = tk.y;
-  const int4 si = P.side_info[slot * 6 + s];
-  const int* od = P.orders + 3 * slot;
-  int d, a, b;
-  side_dirs(s, d, a, b);
-  const int na = od[a] + 1, nb = od[b] + 1, nf = na * nb;
-  const int M1 = si.y & 255, M2 = (si.y >> 8) & 255;
-  const bool swap_r = (si.x & 2) && (((si.x >> 2) & 7) & 4);
-  const int ma = (swap_r ? M2 : M1) + 1, mb = (swap_r ? M1 : M2) + 1, nm = ma * mb;
-  const double* T1 = P.tables + OFF_T + ((na - 1) * 8 + (ma - 1)) * 64;
-  const double* T2 = P.tables + OFF_T + ((nb - 1) * 8 + (mb - 1)) * 64;
-  const double* src = own + P.side_off[slot * 6 + s] * C;
-  double* dst = mort + (long long)si.w * C;
-  warp_projC<C>(na, nb, T1, ma, T2, mb, scr[warp][0], scr[warp][1],
-                [&](int c, int k) { return src[(long long)c * nf + k]; },
-                [&](int c, int k, double x) { dst[(long long)c * nm + k] = x; });
-}
-
 // L2 projection of a nonconforming face's mortar values back onto one side
 // (left or right, own order; the right side negated and re-oriented): one
-// warp per (face, side), all components at once (warp_projC).
+// warp per (face, side), all components on the FP64 tensor cores
+// (warp_proj_mma).
 template <int C>
 __global__ void __launch_bounds__(128) k_down(DevPlan P, double* __restrict__ dst) {
-  __shared__ double scr[4][2][C * 64];
   const int warp = threadIdx.x >> 5;
   const int task = blockIdx.x * 4 + warp;
   if (task >= P.ndown) return;
@@ -154,17 +126,15 @@ __global__ void __launch_bounds__(128) k_down(DevPlan P, double* __restrict__ ds
   const double* T2 = P.tables + OFF_T + (M2 * 8 + o2) * 64;
   const int nf = (o1 + 1) * (o2 + 1);
   double* out = dst + P.side_off[slot * 6 + side] * C;
+  const auto ld = [&](int c, int a, int b) { return src[(long long)c * nm + a + (M1 + 1) * b]; };
   if (!right)
-    warp_projC<C>(M1 + 1, M2 + 1, T1, o1 + 1, T2, o2 + 1, scr[warp][0], scr[warp][1],
-                  [&](int c, int k) { return src[(long long)c * nm + k]; },
-                  [&](int c, int k, double x) { out[(long long)c * nf + k] = x; });
+    warp_proj_mma<C>(M1 + 1, M2 + 1, T1, o1 + 1, T2, o2 + 1, ld,
+                     [&](int c, int A, int B, double x) { out[(long long)c * nf + A + (o1 + 1) * B] = x; });
   else
-    warp_projC<C>(M1 + 1, M2 + 1, T1, o1 + 1, T2, o2 + 1, scr[warp][0], scr[warp][1],
-                  [&](int c, int k) { return src[(long long)c * nm + k]; },
-                  [&](int c, int k, double x) {
-                    const int a = k % (o1 + 1), b = k / (o1 + 1);
-                    out[(long long)c * nf + right_index(a, b, o1, o2, orient)] = -x;
-                  });
+    warp_proj_mma<C>(M1 + 1, M2 + 1, T1, o1 + 1, T2, o2 + 1, ld,
+                     [&](int c, int A, int B, double x) {
+                       out[(long long)c * nf + right_index(A, B, o1, o2, orient)] = -x;
+                     });
 }
 
 // Side kernel: item = (slot, side, kind [-1 = isolated], ghost offset).

@@ -62,32 +62,29 @@ __device__ __forceinline__ void side_mortar_dims(int4 si, int& ma, int& mb) {
 // Side traces of C components for every side of a work item, one warp per
 // side.  Own-order sides: lanes over face nodes (coalesced) into ``own``.
 // Nonconforming sides of a coupled evaluation: the own trace is interpolated
-// onto the side's mortar (own frame) in CH-component chunks through
-// warp_projC and written to ``mort`` at the side's mortar-trace offset, so
-// the face kernels stay pointwise.  vol(e, c, off) reads the volume array.
-template <int C, int CH, class Vol>
+// onto the side's mortar (own frame) on the FP64 tensor cores (warp_proj_mma,
+// reading the face layer through vol()) and written to ``mort`` at the side's
+// mortar-trace offset, so the face kernels stay pointwise.
+template <int C, class Vol>
 __device__ __forceinline__ void item_side_traces(const DevPlan& P, int slot0, int E, int coupled,
                                                  const int np[3], const int strides[3],
                                                  const double (*bnd)[16], double* own, double* mort,
-                                                 double* scratch /* per block: 8 warps x 2*CH*64 */,
                                                  Vol vol) {
   const bool lgl = P.family == 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* s_in = scratch + warp * 2 * CH * 64;
-  double* s_tmp = s_in + CH * 64;
   for (int task = warp; task < E * 6; task += ELEM_THREADS / 32) {
     const int e = task / 6, s = task % 6, slot = slot0 + e;
     int d, a, b;
     side_dirs(s, d, a, b);
-    const int na = np[a], nb = np[b], nf = na * nb;
-    const int last = (s & 1) ? (np[d] - 1) * strides[d] : 0;
+    const int na = np[a], nb = np[b], nf = na * nb, nd = np[d];
+    const int sa = strides[a], sb = strides[b], sd = strides[d];
+    const int last = (s & 1) ? (nd - 1) * sd : 0;
     const double* row = &bnd[d][(s & 1) * 8];
-    auto tr = [&](int c, int k) -> double {
-      const int ib = k / na, ia = k - ib * na;
-      const int off0 = ia * strides[a] + ib * strides[b];
+    auto tr = [&](int c, int ia, int ib) -> double {
+      const int off0 = ia * sa + ib * sb;
       if (lgl) return vol(e, c, off0 + last);
       double acc = 0.0;
-      for (int m = 0; m < np[d]; ++m) acc += row[m] * vol(e, c, off0 + m * strides[d]);
+      for (int m = 0; m < nd; ++m) acc += row[m] * vol(e, c, off0 + m * sd);
       return acc;
     };
     const int4 si = P.side_info[slot * 6 + s];
@@ -98,17 +95,15 @@ __device__ __forceinline__ void item_side_traces(const DevPlan& P, int slot0, in
       const double* T1 = P.tables + OFF_T + ((na - 1) * 8 + (ma - 1)) * 64;
       const double* T2 = P.tables + OFF_T + ((nb - 1) * 8 + (mb - 1)) * 64;
       double* dst = mort + (long long)si.w * C;
-#pragma unroll 1
-      for (int c0 = 0; c0 < C; c0 += CH)
-        warp_projC<CH>(na, nb, T1, ma, T2, mb, s_in, s_tmp,
-                       [&](int c, int k) { return c0 + c < C ? tr(c0 + c, k) : 0.0; },
-                       [&](int c, int k, double x) {
-                         if (c0 + c < C) dst[(long long)(c0 + c) * nm + k] = x;
-                       });
+      warp_proj_mma<C>(na, nb, T1, ma, T2, mb, tr, [&](int c, int A, int B, double x) {
+        dst[(long long)c * nm + A + ma * B] = x;
+      });
     } else {
       double* dst = own + P.side_off[slot * 6 + s] * C;
-      for (int k = lane; k < nf; k += 32)
-        for (int c = 0; c < C; ++c) dst[(long long)c * nf + k] = tr(c, k);
+      for (int k = lane; k < nf; k += 32) {
+        const int ib = k / na, ia = k - ib * na;
+        for (int c = 0; c < C; ++c) dst[(long long)c * nf + k] = tr(c, ia, ib);
+      }
     }
   }
 }
@@ -117,7 +112,6 @@ template <int NV>
 __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const double* __restrict__ Q,
                                                           int coupled) {
   __shared__ double sb[3][16];
-  __shared__ double scratch[ELEM_THREADS / 32 * 2 * NV * 64];
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.orders + 3 * wi.x;
   const int No[3] = {od[0], od[1], od[2]};
@@ -127,7 +121,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
   const int np[3] = {No[0] + 1, No[1] + 1, No[2] + 1};
   const int n = np[0] * np[1] * np[2];
   const int strides[3] = {1, np[0], np[0] * np[1]};
-  item_side_traces<NV, NV>(P, wi.x, wi.y, coupled, np, strides, sb, P.qtr, P.qtrm, scratch,
+  item_side_traces<NV>(P, wi.x, wi.y, coupled, np, strides, sb, P.qtr, P.qtrm,
                            [&](int e, int c, int off) {
                              return Q[(P.node_off[wi.x + e] * NV) + (long long)c * n + off];
                            });
@@ -329,12 +323,10 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
   __syncthreads();
   // gradient traces on the six sides (own order, or mortar order when nonconforming)
   {
-    constexpr int CH = NG < 2 ? NG : 2;
-    __shared__ double scratch[ELEM_THREADS / 32 * 2 * CH * 64];
     const int np[3] = {n1p, n2p, n3p};
     const int strides[3] = {1, n1p, n1p * n2p};
-    item_side_traces<NG, CH>(P, wi.x, wi.y, coupled, np, strides, T.bnd, P.gtr, P.gtrm, scratch,
-                             [&](int e, int c, int off) { return G[c * tot + e * n + off]; });
+    item_side_traces<NG>(P, wi.x, wi.y, coupled, np, strides, T.bnd, P.gtr, P.gtrm,
+                         [&](int e, int c, int off) { return G[c * tot + e * n + off]; });
   }
 }
 
