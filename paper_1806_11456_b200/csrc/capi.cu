@@ -393,7 +393,22 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   UP(side_info_i, desc->side_info, 4 * 6 * ns);
   UP(up_i, desc->up, 2 * desc->nup);
   UP(face_m_off, reinterpret_cast<const long long*>(desc->face_m_off), desc->nfaces);
-  UP(down_i, desc->down, 2 * desc->ndown);
+  {
+    // packed down-projection task descriptors (one load per task)
+    std::vector<int4> dn(static_cast<size_t>(desc->ndown));
+    for (int k = 0; k < desc->ndown; ++k) {
+      const int f = desc->down[2 * k], right = desc->down[2 * k + 1] != 0;
+      const int* fi = desc->face_info + 12 * f;
+      const int slot = right ? fi[2] : fi[0], side = right ? fi[3] : fi[1];
+      const int o1 = right ? fi[7] : fi[5], o2 = right ? fi[8] : fi[6];
+      dn[k] = make_int4(static_cast<int>(desc->face_m_off[f]),
+                        static_cast<int>(desc->side_off[6 * slot + side]),
+                        fi[9] | fi[10] << 3 | o1 << 6 | o2 << 9 | fi[4] << 12 | right << 15, 0);
+    }
+    int4* dn_d = nullptr;
+    if (!rc && !dn.empty()) rc = p->mem.upload(dn.data(), dn.size(), &dn_d);
+    down_i = reinterpret_cast<int*>(dn_d);
+  }
   UP(bface_info, desc->bface_info, 4 * desc->nbfaces);
   UP(ghost_off, reinterpret_cast<const long long*>(desc->ghost_off), desc->nbfaces);
   UP(ghost, desc->ghost, desc->ghost_len);
@@ -423,7 +438,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.up = reinterpret_cast<const int2*>(up_i);
   d.face_m_off = face_m_off;
   d.ndown = desc->ndown;
-  d.down = reinterpret_cast<const int2*>(down_i);
+  d.down = reinterpret_cast<const int4*>(down_i);
 
   {
     int iso = ns > 0 ? p->orders_h[0] : -1;

@@ -61,7 +61,9 @@ struct DevPlan {
   int nup;
   const int2* up;                // (slot, side) up-projection tasks (nonconforming sides)
   int ndown;
-  const int2* down;              // (face, is_right) down-projection tasks
+  // down-projection tasks: x = mortar-surface node offset, y = side node offset,
+  // z = M1 | M2<<3 | o1<<6 | o2<<9 | orient<<12 | is_right<<15 (aligned own orders)
+  const int4* down;
   // scratch (device)
   double* msurf;  // [mortar_nodes][max(nv, 3*ngv)] mortar surface values (left frame)
   double* qtrm;   // mortar-order Q traces of nonconforming sides (own frame)
@@ -173,6 +175,16 @@ __device__ __forceinline__ void warp_proj_mma(int na, int nb, const double* __re
       if (2 * q + 1 < ma) st(c, 2 * q + 1, g, o1);
     }
   }
+}
+
+// Bulk prefetch of a global span into L2 (one instruction, issued by one
+// thread): loads that follow the span's first use then hit L2.
+__device__ __forceinline__ void l2_prefetch_span(const void* p, size_t bytes) {
+  if (bytes == 0) return;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<unsigned>(e - a))
+               : "memory");
 }
 
 // face coordinates of a side: normal direction and the two tangential ones

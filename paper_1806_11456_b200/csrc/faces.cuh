@@ -114,18 +114,16 @@ __global__ void __launch_bounds__(128) k_down(DevPlan P, double* __restrict__ ds
   const int warp = threadIdx.x >> 5;
   const int task = blockIdx.x * 4 + warp;
   if (task >= P.ndown) return;
-  const int2 dt = P.down[task];
-  const int* fi = P.face_info + 12 * dt.x;
-  const int M1 = fi[9], M2 = fi[10], orient = fi[4];
+  const int4 tk = P.down[task];
+  const int M1 = tk.z & 7, M2 = (tk.z >> 3) & 7, o1 = (tk.z >> 6) & 7, o2 = (tk.z >> 9) & 7;
+  const int orient = (tk.z >> 12) & 7;
+  const bool right = (tk.z >> 15) & 1;
   const int nm = (M1 + 1) * (M2 + 1);
-  const double* src = P.msurf + P.face_m_off[dt.x] * C;
-  const bool right = dt.y != 0;
-  const int o1 = right ? fi[7] : fi[5], o2 = right ? fi[8] : fi[6];   // aligned own orders
-  const int slot = right ? fi[2] : fi[0], side = right ? fi[3] : fi[1];
+  const double* src = P.msurf + (long long)tk.x * C;
   const double* T1 = P.tables + OFF_T + (M1 * 8 + o1) * 64;
   const double* T2 = P.tables + OFF_T + (M2 * 8 + o2) * 64;
   const int nf = (o1 + 1) * (o2 + 1);
-  double* out = dst + P.side_off[slot * 6 + side] * C;
+  double* out = dst + (long long)tk.y * C;
   const auto ld = [&](int c, int a, int b) { return src[(long long)c * nm + a + (M1 + 1) * b]; };
   if (!right)
     warp_proj_mma<C>(M1 + 1, M2 + 1, T1, o1 + 1, T2, o2 + 1, ld,

@@ -108,6 +108,17 @@ __device__ __forceinline__ void item_side_traces(const DevPlan& P, int slot0, in
   }
 }
 
+// L2 bulk prefetch of a work item's per-side surface span ([C][nf] per side,
+// contiguous over the item's slots and sides), read late by the scatter.
+template <int C>
+__device__ __forceinline__ void prefetch_item_surface(const DevPlan& P, const double* surf, int2 wi,
+                                                      int N1, int N2) {
+  if (threadIdx.x != 0 || surf == nullptr) return;
+  const long long s0 = P.side_off[wi.x * 6];
+  const long long s1 = P.side_off[(wi.x + wi.y - 1) * 6 + 5] + (long long)(N1 + 1) * (N2 + 1);
+  l2_prefetch_span(surf + s0 * C, static_cast<size_t>(s1 - s0) * C * sizeof(double));
+}
+
 template <int NV>
 __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const double* __restrict__ Q,
                                                           int coupled) {
@@ -146,6 +157,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.orders + 3 * wi.x;
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
+  prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
   load_tables(P, N1, N2, N3, T);
   if (threadIdx.x == 0) {
     int a = 1;
@@ -356,6 +368,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.orders + 3 * wi.x;
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
+  prefetch_item_surface<NV>(P, P.fsurf, wi, N1, N2);
   load_tables(P, N1, N2, N3, T);
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
