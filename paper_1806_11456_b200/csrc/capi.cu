@@ -340,6 +340,10 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   if (desc->law < 0 || desc->law > 2) return fail(TDG_E_CONFIG, "unknown law id");
   if (desc->tables_len != TABLES_LEN) return fail(TDG_E_CONFIG, "spectral table length mismatch");
   if (desc->nslots < 0) return fail(TDG_E_ARG, "negative slot count");
+  // packed face / down-projection descriptors hold node offsets as int32
+  if (desc->side_nodes > INT32_MAX || desc->mtr_nodes > INT32_MAX || desc->mortar_nodes > INT32_MAX ||
+      desc->face_geo_len > INT32_MAX)
+    return fail(TDG_E_CONFIG, "plan too large: side / mortar offsets exceed int32");
   auto* p = new tdg_plan();
   p->nv = law_nv(desc->law);
   p->ngv = law_ngv(desc->law);
@@ -405,6 +409,22 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
                         static_cast<int>(desc->side_off[6 * slot + side]),
                         fi[9] | fi[10] << 3 | o1 << 6 | o2 << 9 | fi[4] << 12 | right << 15, 0);
     }
+    std::vector<int4> fdv(2 * static_cast<size_t>(desc->nfaces));
+    for (int f = 0; f < desc->nfaces; ++f) {
+      const int* fi = desc->face_info + 12 * f;
+      const int M1 = fi[9], M2 = fi[10];
+      const bool conf = fi[5] == M1 && fi[6] == M2 && fi[7] == M1 && fi[8] == M2;
+      const int kl = 6 * fi[0] + fi[1], kr = 6 * fi[2] + fi[3];
+      const long long tl = conf ? desc->side_off[kl] : desc->side_info[4 * kl + 3];
+      const long long tr = conf ? desc->side_off[kr] : desc->side_info[4 * kr + 3];
+      fdv[2 * f] = make_int4(static_cast<int>(tl), static_cast<int>(tr),
+                             M1 | M2 << 3 | fi[4] << 6 | (conf ? 1 : 0) << 9,
+                             static_cast<int>(desc->face_geo_off[f]));
+      fdv[2 * f + 1] = make_int4(static_cast<int>(desc->face_m_off[f]), 0, 0, 0);
+    }
+    int4* fd_d = nullptr;
+    if (!rc && !fdv.empty()) rc = p->mem.upload(fdv.data(), fdv.size(), &fd_d);
+    d.fdesc = fd_d;
     int4* dn_d = nullptr;
     if (!rc && !dn.empty()) rc = p->mem.upload(dn.data(), dn.size(), &dn_d);
     down_i = reinterpret_cast<int*>(dn_d);

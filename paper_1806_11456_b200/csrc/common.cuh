@@ -61,6 +61,11 @@ struct DevPlan {
   int nup;
   const int2* up;                // (slot, side) up-projection tasks (nonconforming sides)
   int ndown;
+  // per interior face, two int4: [2f] = (left trace offset, right trace offset,
+  // M1 | M2<<3 | orient<<6 | conforming<<9, face-geometry offset), [2f+1].x =
+  // mortar-surface offset (trace offsets: own side arrays when conforming,
+  // mortar traces otherwise)
+  const int4* fdesc;
   // down-projection tasks: x = mortar-surface node offset, y = side node offset,
   // z = M1 | M2<<3 | o1<<6 | o2<<9 | orient<<12 | is_right<<15 (aligned own orders)
   const int4* down;

@@ -37,21 +37,18 @@ __global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
   constexpr int COUT = FLUX ? NV : NG;
   const int f = blockIdx.x;
   const int t = threadIdx.x;
-  const int* fi = P.face_info + 12 * f;
-  const int M1 = fi[9], M2 = fi[10];
+  const int4 fd = P.fdesc[2 * f];
+  const int M1 = fd.z & 7, M2 = (fd.z >> 3) & 7, orient = (fd.z >> 6) & 7;
+  const bool conf = (fd.z >> 9) & 1;
   const int nm = (M1 + 1) * (M2 + 1);
   if (t >= nm) return;
-  const int slotL = fi[0], sideL = fi[1], slotR = fi[2], sideR = fi[3], orient = fi[4];
-  const int L1 = fi[5], L2 = fi[6], R1 = fi[7], R2 = fi[8];
-  const bool conf = (L1 == M1) && (L2 == M2) && (R1 == M1) && (R2 == M2);
   const int A = t % (M1 + 1), B = t / (M1 + 1);
   const int kR = right_index(A, B, M1, M2, orient);
   // conforming: own-order traces; nonconforming: mortar traces (item_side_traces)
   const double* qsrc = conf ? P.qtr : P.qtrm;
   const double* gsrc = conf ? P.gtr : P.gtrm;
-  const long long tL = conf ? P.side_off[slotL * 6 + sideL] : P.side_info[slotL * 6 + sideL].w;
-  const long long tR = conf ? P.side_off[slotR * 6 + sideR] : P.side_info[slotR * 6 + sideR].w;
-  const double* geo = P.face_geo + P.face_geo_off[f];
+  const long long tL = fd.x, tR = fd.y;
+  const double* geo = P.face_geo + fd.w;
   const double sigma = geo[t];
   const double nrm[3] = {geo[nm + t], geo[2 * nm + t], geo[3 * nm + t]};
   double ql[NV], qr[NV];
@@ -91,15 +88,15 @@ __global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
   }
   if (conf) {
     double* dst = FLUX ? P.fsurf : P.lsurf;
-    const long long oL = P.side_off[slotL * 6 + sideL] * COUT;
-    const long long oR = P.side_off[slotR * 6 + sideR] * COUT;
+    const long long oL = tL * COUT;
+    const long long oR = tR * COUT;
 #pragma unroll
     for (int c = 0; c < COUT; ++c) {
       dst[oL + (long long)c * nm + t] = val[c];
       dst[oR + (long long)c * nm + kR] = -val[c];
     }
   } else {
-    double* dst = P.msurf + P.face_m_off[f] * COUT;
+    double* dst = P.msurf + (long long)P.fdesc[2 * f + 1].x * COUT;
 #pragma unroll
     for (int c = 0; c < COUT; ++c) dst[(long long)c * nm + t] = val[c];
   }
