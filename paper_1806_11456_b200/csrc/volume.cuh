@@ -119,6 +119,16 @@ __device__ __forceinline__ void prefetch_item_surface(const DevPlan& P, const do
   l2_prefetch_span(surf + s0 * C, static_cast<size_t>(s1 - s0) * C * sizeof(double));
 }
 
+// L2 bulk prefetch of a work item's per-node span of a C-component field
+// (the item's slots are contiguous), issued by thread ``who``.
+template <int C>
+__device__ __forceinline__ void prefetch_item_nodes(const DevPlan& P, const double* x, int2 wi,
+                                                    int who) {
+  if (threadIdx.x != who || x == nullptr) return;
+  const long long n0 = P.node_off[wi.x], n1 = P.node_off[wi.x + wi.y];
+  l2_prefetch_span(x + n0 * C, static_cast<size_t>(n1 - n0) * C * sizeof(double));
+}
+
 template <int NV>
 __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const double* __restrict__ Q,
                                                           int coupled) {
@@ -369,6 +379,9 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   const int* od = P.orders + 3 * wi.x;
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
   prefetch_item_surface<NV>(P, P.fsurf, wi, N1, N2);
+  // epilogue inputs, read after the contraction
+  if (MODE != MODE_F) prefetch_item_nodes<NV>(P, MODE == MODE_A ? A.X : A.S, wi, 32);
+  if (MODE == MODE_RK && A.stage != 0) prefetch_item_nodes<NV>(P, A.W, wi, 64);
   load_tables(P, N1, N2, N3, T);
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
