@@ -527,6 +527,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     return rc;
   }
   d.nwork = static_cast<int>(work.size());
+  d.nsm = nsm_attr;
   d.work = work_d;
   d.nside_iso = static_cast<int>(iso.size());
   d.side_iso = iso_d;

@@ -48,6 +48,7 @@ struct DevPlan {
   // element work items: (first slot, count), uniform orders inside an item
   int nwork;
   const int2* work;
+  int nsm;        // SMs: element kernels prefetch the item one wave ahead (L2)
   // side work items for side kernels: (slot, side | kind<<8), ghost offset
   int nside_iso;
   const int4* side_iso;      // isolated: every side of every element

@@ -37,6 +37,24 @@ __global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
   constexpr int COUT = FLUX ? NV : NG;
   const int f = blockIdx.x;
   const int t = threadIdx.x;
+  if (t == 0) {
+    // L2 prefetch of the face about one wave ahead (8 resident blocks per SM)
+    const int fa = f + 8 * P.nsm;
+    if (fa < P.nfaces) {
+      const int4 fn = P.fdesc[2 * fa];
+      const int mn = ((fn.z & 7) + 1) * (((fn.z >> 3) & 7) + 1);
+      const bool cn = (fn.z >> 9) & 1;
+      const double* qs = cn ? P.qtr : P.qtrm;
+      l2_prefetch_span(qs + (long long)fn.x * NV, sizeof(double) * mn * NV);
+      l2_prefetch_span(qs + (long long)fn.y * NV, sizeof(double) * mn * NV);
+      l2_prefetch_span(P.face_geo + fn.w, sizeof(double) * mn * 4);
+      if (FLUX && L::viscous(P.prm)) {
+        const double* gs = cn ? P.gtr : P.gtrm;
+        l2_prefetch_span(gs + (long long)fn.x * NG, sizeof(double) * mn * NG);
+        l2_prefetch_span(gs + (long long)fn.y * NG, sizeof(double) * mn * NG);
+      }
+    }
+  }
   const int4 fd = P.fdesc[2 * f];
   const int M1 = fd.z & 7, M2 = (fd.z >> 3) & 7, orient = (fd.z >> 6) & 7;
   const bool conf = (fd.z >> 9) & 1;
@@ -111,6 +129,15 @@ __global__ void __launch_bounds__(128) k_down(DevPlan P, double* __restrict__ ds
   const int warp = threadIdx.x >> 5;
   const int task = blockIdx.x * 4 + warp;
   if (task >= P.ndown) return;
+  {
+    // L2 prefetch of the task about one wave ahead (10 resident blocks per SM)
+    const int ta = task + 4 * 10 * P.nsm;
+    if ((threadIdx.x & 31) == 0 && ta < P.ndown) {
+      const int4 tn = P.down[ta];
+      const int mn = ((tn.z & 7) + 1) * (((tn.z >> 3) & 7) + 1);
+      l2_prefetch_span(P.msurf + (long long)tn.x * C, sizeof(double) * mn * C);
+    }
+  }
   const int4 tk = P.down[task];
   const int M1 = tk.z & 7, M2 = (tk.z >> 3) & 7, o1 = (tk.z >> 6) & 7, o2 = (tk.z >> 9) & 7;
   const int orient = (tk.z >> 12) & 7;

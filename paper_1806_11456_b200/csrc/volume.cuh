@@ -129,11 +129,23 @@ __device__ __forceinline__ void prefetch_item_nodes(const DevPlan& P, const doub
   l2_prefetch_span(x + n0 * C, static_cast<size_t>(n1 - n0) * C * sizeof(double));
 }
 
+// The work item per_sm * nsm blocks ahead of this block (blocks start in
+// index order: with per_sm resident blocks per SM it runs about one wave
+// later), or wi.y == 0 if none.
+__device__ __forceinline__ int2 item_ahead(const DevPlan& P, int per_sm) {
+  const int b = blockIdx.x + per_sm * P.nsm;
+  return b < P.nwork ? P.work[b] : make_int2(0, 0);
+}
+
 template <int NV>
 __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const double* __restrict__ Q,
                                                           int coupled) {
   __shared__ double sb[3][16];
   const int2 wi = P.work[blockIdx.x];
+  {
+    const int2 wn = item_ahead(P, 4);
+    if (wn.y > 0) prefetch_item_nodes<NV>(P, Q, wn, 0);
+  }
   const int* od = P.orders + 3 * wi.x;
   const int No[3] = {od[0], od[1], od[2]};
   for (int u = threadIdx.x; u < 48; u += blockDim.x)
