@@ -528,6 +528,15 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   }
   d.nwork = static_cast<int>(work.size());
   d.nsm = nsm_attr;
+  {
+    auto knob = [](const char* name, int dflt) {
+      const char* v = getenv(name);
+      return v ? atoi(v) : dflt;
+    };
+    d.pf_trace = knob("TDG_PF_TRACE", 2);
+    d.pf_face = knob("TDG_PF_FACE", 4);
+    d.pf_down = knob("TDG_PF_DOWN", 5);
+  }
   d.work = work_d;
   d.nside_iso = static_cast<int>(iso.size());
   d.side_iso = iso_d;

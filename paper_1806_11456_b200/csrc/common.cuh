@@ -48,7 +48,8 @@ struct DevPlan {
   // element work items: (first slot, count), uniform orders inside an item
   int nwork;
   const int2* work;
-  int nsm;        // SMs: element kernels prefetch the item one wave ahead (L2)
+  int nsm;        // SMs: kernels prefetch the work about one wave ahead (L2)
+  int pf_trace, pf_face, pf_down;   // look-ahead distances, blocks per SM
   // side work items for side kernels: (slot, side | kind<<8), ghost offset
   int nside_iso;
   const int4* side_iso;      // isolated: every side of every element

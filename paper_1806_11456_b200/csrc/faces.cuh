@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
   const int t = threadIdx.x;
   if (t == 0) {
     // L2 prefetch of the face about one wave ahead (8 resident blocks per SM)
-    const int fa = f + 8 * P.nsm;
+    const int fa = f + P.pf_face * P.nsm;
     if (fa < P.nfaces) {
       const int4 fn = P.fdesc[2 * fa];
       const int mn = ((fn.z & 7) + 1) * (((fn.z >> 3) & 7) + 1);
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(128) k_down(DevPlan P, double* __restrict__ ds
   if (task >= P.ndown) return;
   {
     // L2 prefetch of the task about one wave ahead (10 resident blocks per SM)
-    const int ta = task + 4 * 10 * P.nsm;
+    const int ta = task + 4 * P.pf_down * P.nsm;
     if ((threadIdx.x & 31) == 0 && ta < P.ndown) {
       const int4 tn = P.down[ta];
       const int mn = ((tn.z & 7) + 1) * (((tn.z >> 3) & 7) + 1);

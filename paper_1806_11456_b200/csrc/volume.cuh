@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
   __shared__ double sb[3][16];
   const int2 wi = P.work[blockIdx.x];
   {
-    const int2 wn = item_ahead(P, 4);
+    const int2 wn = item_ahead(P, P.pf_trace);
     if (wn.y > 0) prefetch_item_nodes<NV>(P, Q, wn, 0);
   }
   const int* od = P.orders + 3 * wi.x;
