@@ -91,6 +91,9 @@ typedef struct {
    * w = offset (nodes) of the side's mortar-order traces when nonconforming */
   const int32_t* side_info;    /* [nslots*6*4] */
   int64_t mtr_nodes;           /* total mortar-trace nodes of nonconforming sides */
+  /* Reserved (ABI-stable, not read since nonconforming faces are projected
+     in registers, one warp per face): mortar-array offsets and the up / down
+     projection task lists.  Callers may pass zeros / NULL. */
   const int64_t* face_m_off;   /* [nfaces] mortar-array offset (nodes), -1 when conforming */
   int64_t mortar_nodes;        /* total mortar nodes of nonconforming faces */
   int32_t nup;                 /* up-projection tasks */

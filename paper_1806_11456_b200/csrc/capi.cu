@@ -120,7 +120,7 @@ struct KTimer {
 };
 
 const char* const KNAMES[TDG_K_COUNT] = {"trace_q", "side_lift", "face_lift", "vol_lift", "side_flux",
-                                         "face_flux", "vol_flux", "element_dt", "norm", "transfer", "down_proj", "up_proj"};
+                                         "face_flux", "vol_flux", "element_dt", "norm", "transfer", "mortar_face", "up_proj"};
 
 __global__ void k_fill(double* p, double v, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -231,19 +231,23 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
       LAUNCH_CHECK("k_side");
     }
     if (!isolated && d.nfaces > 0) {
-      KTimer kt(flux ? TDG_K_FACE_FLUX : TDG_K_FACE_LIFT, st);
-      if (flux)
-        k_face<LAW, true><<<d.nfaces, FACE_THREADS, 0, st>>>(d);
-      else
-        k_face<LAW, false><<<d.nfaces, FACE_THREADS, 0, st>>>(d);
-      LAUNCH_CHECK("k_face");
-      if (d.ndown > 0) {
+      if (d.ncface > 0) {
+        KTimer kt(flux ? TDG_K_FACE_FLUX : TDG_K_FACE_LIFT, st);
+        if (flux)
+          k_face<LAW, true><<<d.ncface, FACE_THREADS, 0, st>>>(d);
+        else
+          k_face<LAW, false><<<d.ncface, FACE_THREADS, 0, st>>>(d);
+        LAUNCH_CHECK("k_face");
+      }
+      if (d.nmface > 0) {
+        // nonconforming faces: pointwise values and both down-projections in one warp
+        // (timer class TDG_K_DOWN = "mortar_face")
         KTimer kd(TDG_K_DOWN, st);
         if (flux)
-          k_down<L::NV><<<(d.ndown + 3) / 4, 128, 0, st>>>(d, d.fsurf);
+          k_mortar<LAW, true><<<(d.nmface + 3) / 4, 128, 0, st>>>(d);
         else
-          k_down<3 * L::NGV><<<(d.ndown + 3) / 4, 128, 0, st>>>(d, d.lsurf);
-        LAUNCH_CHECK("k_down");
+          k_mortar<LAW, false><<<(d.nmface + 3) / 4, 128, 0, st>>>(d);
+        LAUNCH_CHECK("k_mortar");
       }
     }
     return TDG_OK;
@@ -341,7 +345,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   if (desc->tables_len != TABLES_LEN) return fail(TDG_E_CONFIG, "spectral table length mismatch");
   if (desc->nslots < 0) return fail(TDG_E_ARG, "negative slot count");
   // packed face / down-projection descriptors hold node offsets as int32
-  if (desc->side_nodes > INT32_MAX || desc->mtr_nodes > INT32_MAX || desc->mortar_nodes > INT32_MAX ||
+  if (desc->side_nodes > INT32_MAX || desc->mtr_nodes > INT32_MAX ||
       desc->face_geo_len > INT32_MAX)
     return fail(TDG_E_CONFIG, "plan too large: side / mortar offsets exceed int32");
   auto* p = new tdg_plan();
@@ -392,24 +396,13 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   UP(face_geo_off, reinterpret_cast<const long long*>(desc->face_geo_off), desc->nfaces);
   UP(face_geo, desc->face_geo, desc->face_geo_len);
   int* side_info_i;
-  long long* face_m_off;
-  int *down_i, *up_i;
   UP(side_info_i, desc->side_info, 4 * 6 * ns);
-  UP(up_i, desc->up, 2 * desc->nup);
-  UP(face_m_off, reinterpret_cast<const long long*>(desc->face_m_off), desc->nfaces);
   {
-    // packed down-projection task descriptors (one load per task)
-    std::vector<int4> dn(static_cast<size_t>(desc->ndown));
-    for (int k = 0; k < desc->ndown; ++k) {
-      const int f = desc->down[2 * k], right = desc->down[2 * k + 1] != 0;
-      const int* fi = desc->face_info + 12 * f;
-      const int slot = right ? fi[2] : fi[0], side = right ? fi[3] : fi[1];
-      const int o1 = right ? fi[7] : fi[5], o2 = right ? fi[8] : fi[6];
-      dn[k] = make_int4(static_cast<int>(desc->face_m_off[f]),
-                        static_cast<int>(desc->side_off[6 * slot + side]),
-                        fi[9] | fi[10] << 3 | o1 << 6 | o2 << 9 | fi[4] << 12 | right << 15, 0);
-    }
+    // packed per-face descriptors and the conforming / nonconforming face lists
+    // (face_m_off, mortar_nodes, up and down of the descriptor are not read:
+    // nonconforming faces are projected in registers by k_mortar)
     std::vector<int4> fdv(2 * static_cast<size_t>(desc->nfaces));
+    std::vector<int> cfv, mfv;
     for (int f = 0; f < desc->nfaces; ++f) {
       const int* fi = desc->face_info + 12 * f;
       const int M1 = fi[9], M2 = fi[10];
@@ -420,14 +413,20 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
       fdv[2 * f] = make_int4(static_cast<int>(tl), static_cast<int>(tr),
                              M1 | M2 << 3 | fi[4] << 6 | (conf ? 1 : 0) << 9,
                              static_cast<int>(desc->face_geo_off[f]));
-      fdv[2 * f + 1] = make_int4(static_cast<int>(desc->face_m_off[f]), 0, 0, 0);
+      fdv[2 * f + 1] = make_int4(0, static_cast<int>(desc->side_off[kl]), static_cast<int>(desc->side_off[kr]),
+                                 fi[5] | fi[6] << 3 | fi[7] << 6 | fi[8] << 9);
+      (conf ? cfv : mfv).push_back(f);
     }
+    int *cf_d = nullptr, *mf_d = nullptr;
+    if (!rc && !cfv.empty()) rc = p->mem.upload(cfv.data(), cfv.size(), &cf_d);
+    if (!rc && !mfv.empty()) rc = p->mem.upload(mfv.data(), mfv.size(), &mf_d);
+    d.ncface = static_cast<int>(cfv.size());
+    d.nmface = static_cast<int>(mfv.size());
+    d.cface = cf_d;
+    d.mface = mf_d;
     int4* fd_d = nullptr;
     if (!rc && !fdv.empty()) rc = p->mem.upload(fdv.data(), fdv.size(), &fd_d);
     d.fdesc = fd_d;
-    int4* dn_d = nullptr;
-    if (!rc && !dn.empty()) rc = p->mem.upload(dn.data(), dn.size(), &dn_d);
-    down_i = reinterpret_cast<int*>(dn_d);
   }
   UP(bface_info, desc->bface_info, 4 * desc->nbfaces);
   UP(ghost_off, reinterpret_cast<const long long*>(desc->ghost_off), desc->nbfaces);
@@ -454,11 +453,6 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.ghost_off = ghost_off;
   d.ghost = ghost;
   d.side_info = reinterpret_cast<const int4*>(side_info_i);
-  d.nup = desc->nup;
-  d.up = reinterpret_cast<const int2*>(up_i);
-  d.face_m_off = face_m_off;
-  d.ndown = desc->ndown;
-  d.down = reinterpret_cast<const int4*>(down_i);
 
   {
     int iso = ns > 0 ? p->orders_h[0] : -1;
@@ -509,13 +503,11 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
 
   const int NG = 3 * p->ngv;
   const size_t tn = static_cast<size_t>(desc->mtr_nodes);
-  const size_t mn = static_cast<size_t>(desc->mortar_nodes);
-  double *qtr, *lsurf = nullptr, *gtr = nullptr, *fsurf, *grad = nullptr, *msurf = nullptr;
+  double *qtr, *lsurf = nullptr, *gtr = nullptr, *fsurf, *grad = nullptr;
   double *qtrm = nullptr, *gtrm = nullptr;
   if (!rc) rc = p->mem.zeros(sn * p->nv, &qtr);
   if (!rc) rc = p->mem.zeros(tn * p->nv, &qtrm);
   if (!rc) rc = p->mem.zeros(sn * p->nv, &fsurf);
-  if (!rc) rc = p->mem.zeros(mn * std::max(p->nv, p->viscous ? NG : 1), &msurf);
   if (p->viscous) {
     if (!rc) rc = p->mem.zeros(sn * NG, &lsurf);
     if (!rc) rc = p->mem.zeros(sn * NG, &gtr);
@@ -545,7 +537,6 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.qtr = qtr;
   d.qtrm = qtrm;
   d.gtrm = gtrm;
-  d.msurf = msurf;
   d.lsurf = lsurf;
   d.gtr = gtr;
   d.fsurf = fsurf;

@@ -59,20 +59,16 @@ struct DevPlan {
   // y = M1 | M2<<8 (mortar orders, left frame), z = face index (-1: boundary),
   // w = mortar-trace offset (nodes) of a nonconforming side
   const int4* side_info;
-  const long long* face_m_off;   // mortar-surface offset per face (nodes), -1 if conforming
-  int nup;
-  const int2* up;                // (slot, side) up-projection tasks (nonconforming sides)
-  int ndown;
   // per interior face, two int4: [2f] = (left trace offset, right trace offset,
-  // M1 | M2<<3 | orient<<6 | conforming<<9, face-geometry offset), [2f+1].x =
-  // mortar-surface offset (trace offsets: own side arrays when conforming,
-  // mortar traces otherwise)
+  // M1 | M2<<3 | orient<<6 | conforming<<9, face-geometry offset) (trace
+  // offsets: own side arrays when conforming, mortar traces otherwise);
+  // [2f+1] = (0, left side offset, right side offset,
+  // L1 | L2<<3 | R1<<6 | R2<<9 aligned own orders)
   const int4* fdesc;
-  // down-projection tasks: x = mortar-surface node offset, y = side node offset,
-  // z = M1 | M2<<3 | o1<<6 | o2<<9 | orient<<12 | is_right<<15 (aligned own orders)
-  const int4* down;
+  int ncface, nmface;
+  const int* cface;              // conforming interior faces (k_face)
+  const int* mface;              // nonconforming interior faces (k_mortar)
   // scratch (device)
-  double* msurf;  // [mortar_nodes][max(nv, 3*ngv)] mortar surface values (left frame)
   double* qtrm;   // mortar-order Q traces of nonconforming sides (own frame)
   double* gtrm;   // mortar-order gradient traces of nonconforming sides
   double* qtr;    // [side_nodes][nv] own-order Q traces

@@ -24,49 +24,18 @@ __device__ __forceinline__ int right_index(int a, int b, int R1, int R2, int ori
   return (orient & 4) ? (bp + (R2 + 1) * ap) : (ap + (R1 + 1) * bp);
 }
 
-// Interior face, pointwise: one thread per mortar node.  Both sides' traces
-// already live at the mortar order (k_trace_q / k_vol_lift interpolate the
-// nonconforming sides), so no shared memory and no barriers are needed.
-// Conforming faces write the signed per-side own-order surface arrays
-// directly; nonconforming faces write one mortar array (left frame) that
-// k_down projects back onto each side (operators.py:211-217, 257-261, 330-334).
+// Pointwise interface value at mortar node t (left frame; kR = the right
+// side's index of the same node): the BR1 lift g*·n σ (3 ngv values) or the
+// numerical flux (Roe − ½(F_v,L + F_v,R)·n) σ (nv values) (operators.py:
+// 211-217, 257-261, 283-290, 330-334).  Traces come from qsrc/gsrc at trace
+// offsets tL/tR with nm nodes per side.
 template <int LAW, bool FLUX>
-__global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
+__device__ __forceinline__ void face_point(const DevPlan& P, const double* qsrc, const double* gsrc,
+                                           long long tL, long long tR, int nm, int t, int kR,
+                                           const double* geo,
+                                           double* val /* [FLUX ? NV : 3 NGV] */) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
-  constexpr int COUT = FLUX ? NV : NG;
-  const int f = blockIdx.x;
-  const int t = threadIdx.x;
-  if (t == 0) {
-    // L2 prefetch of the face about one wave ahead (8 resident blocks per SM)
-    const int fa = f + P.pf_face * P.nsm;
-    if (fa < P.nfaces) {
-      const int4 fn = P.fdesc[2 * fa];
-      const int mn = ((fn.z & 7) + 1) * (((fn.z >> 3) & 7) + 1);
-      const bool cn = (fn.z >> 9) & 1;
-      const double* qs = cn ? P.qtr : P.qtrm;
-      l2_prefetch_span(qs + (long long)fn.x * NV, sizeof(double) * mn * NV);
-      l2_prefetch_span(qs + (long long)fn.y * NV, sizeof(double) * mn * NV);
-      l2_prefetch_span(P.face_geo + fn.w, sizeof(double) * mn * 4);
-      if (FLUX && L::viscous(P.prm)) {
-        const double* gs = cn ? P.gtr : P.gtrm;
-        l2_prefetch_span(gs + (long long)fn.x * NG, sizeof(double) * mn * NG);
-        l2_prefetch_span(gs + (long long)fn.y * NG, sizeof(double) * mn * NG);
-      }
-    }
-  }
-  const int4 fd = P.fdesc[2 * f];
-  const int M1 = fd.z & 7, M2 = (fd.z >> 3) & 7, orient = (fd.z >> 6) & 7;
-  const bool conf = (fd.z >> 9) & 1;
-  const int nm = (M1 + 1) * (M2 + 1);
-  if (t >= nm) return;
-  const int A = t % (M1 + 1), B = t / (M1 + 1);
-  const int kR = right_index(A, B, M1, M2, orient);
-  // conforming: own-order traces; nonconforming: mortar traces (item_side_traces)
-  const double* qsrc = conf ? P.qtr : P.qtrm;
-  const double* gsrc = conf ? P.gtr : P.gtrm;
-  const long long tL = fd.x, tR = fd.y;
-  const double* geo = P.face_geo + fd.w;
   const double sigma = geo[t];
   const double nrm[3] = {geo[nm + t], geo[2 * nm + t], geo[3 * nm + t]};
   double ql[NV], qr[NV];
@@ -75,7 +44,6 @@ __global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
     ql[v] = qsrc[tL * NV + (long long)v * nm + t];
     qr[v] = qsrc[tR * NV + (long long)v * nm + kR];
   }
-  double val[COUT];
   if (!FLUX) {
     double gl[NGV], gr[NGV];
     L::grad_vars(P.prm, ql, gl);
@@ -104,59 +72,121 @@ __global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
 #pragma unroll
     for (int v = 0; v < NV; ++v) val[v] = F[v] * sigma;
   }
-  if (conf) {
-    double* dst = FLUX ? P.fsurf : P.lsurf;
-    const long long oL = tL * COUT;
-    const long long oR = tR * COUT;
-#pragma unroll
-    for (int c = 0; c < COUT; ++c) {
-      dst[oL + (long long)c * nm + t] = val[c];
-      dst[oR + (long long)c * nm + kR] = -val[c];
+}
+
+// Conforming interior face, pointwise: one thread per face node; both sides'
+// own-order traces align node for node (up to orientation), and the signed
+// values go straight into the per-side own-order surface arrays.
+template <int LAW, bool FLUX>
+__global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
+  using L = Law<LAW>;
+  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
+  constexpr int COUT = FLUX ? NV : NG;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    // L2 prefetch of the face about one wave ahead
+    const int ba = blockIdx.x + P.pf_face * P.nsm;
+    if (ba < P.ncface) {
+      const int4 fn = P.fdesc[2 * (P.nmface ? P.cface[ba] : ba)];
+      const int mn = ((fn.z & 7) + 1) * (((fn.z >> 3) & 7) + 1);
+      l2_prefetch_span(P.qtr + (long long)fn.x * NV, sizeof(double) * mn * NV);
+      l2_prefetch_span(P.qtr + (long long)fn.y * NV, sizeof(double) * mn * NV);
+      l2_prefetch_span(P.face_geo + fn.w, sizeof(double) * mn * 4);
+      if (FLUX && L::viscous(P.prm)) {
+        l2_prefetch_span(P.gtr + (long long)fn.x * NG, sizeof(double) * mn * NG);
+        l2_prefetch_span(P.gtr + (long long)fn.y * NG, sizeof(double) * mn * NG);
+      }
     }
-  } else {
-    double* dst = P.msurf + (long long)P.fdesc[2 * f + 1].x * COUT;
+  }
+  const int f = P.nmface ? P.cface[blockIdx.x] : blockIdx.x;   // all conforming: identity list
+  const int4 fd = P.fdesc[2 * f];
+  const int M1 = fd.z & 7, M2 = (fd.z >> 3) & 7, orient = (fd.z >> 6) & 7;
+  const int nm = (M1 + 1) * (M2 + 1);
+  if (t >= nm) return;
+  const int A = t % (M1 + 1), B = t / (M1 + 1);
+  const int kR = right_index(A, B, M1, M2, orient);
+  const long long tL = fd.x, tR = fd.y;
+  double val[COUT];
+  face_point<LAW, FLUX>(P, P.qtr, P.gtr, tL, tR, nm, t, kR, P.face_geo + fd.w, val);
+  double* dst = FLUX ? P.fsurf : P.lsurf;
+  const long long oL = tL * COUT;
+  const long long oR = tR * COUT;
 #pragma unroll
-    for (int c = 0; c < COUT; ++c) dst[(long long)c * nm + t] = val[c];
+  for (int c = 0; c < COUT; ++c) {
+    dst[oL + (long long)c * nm + t] = val[c];
+    dst[oR + (long long)c * nm + kR] = -val[c];
   }
 }
 
-// L2 projection of a nonconforming face's mortar values back onto one side
-// (left or right, own order; the right side negated and re-oriented): one
-// warp per (face, side), all components on the FP64 tensor cores
-// (warp_proj_mma).
-template <int C>
-__global__ void __launch_bounds__(128) k_down(DevPlan P, double* __restrict__ dst) {
-  const int warp = threadIdx.x >> 5;
+// Nonconforming interior face: one warp per face.  Lane (g, q) evaluates the
+// pointwise interface value at mortar nodes (q, g) and (q+4, g) — exactly the
+// B operand positions of the first projection pass — keeps them in registers
+// and L2-projects them onto both sides on the FP64 tensor cores (the right
+// side negated and re-oriented).  Nothing goes through HBM between the
+// pointwise evaluation and the projections (operators.py:211-217, 330-334).
+template <int LAW, bool FLUX>
+__global__ void __launch_bounds__(128, FLUX ? 4 : 5) k_mortar(DevPlan P) {
+  using L = Law<LAW>;
+  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
+  constexpr int COUT = FLUX ? NV : NG;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int task = blockIdx.x * 4 + warp;
-  if (task >= P.ndown) return;
-  {
-    // L2 prefetch of the task about one wave ahead (10 resident blocks per SM)
-    const int ta = task + 4 * P.pf_down * P.nsm;
-    if ((threadIdx.x & 31) == 0 && ta < P.ndown) {
-      const int4 tn = P.down[ta];
-      const int mn = ((tn.z & 7) + 1) * (((tn.z >> 3) & 7) + 1);
-      l2_prefetch_span(P.msurf + (long long)tn.x * C, sizeof(double) * mn * C);
+  if (task >= P.nmface) return;
+  if (lane == 0) {
+    const int ta = task + 4 * P.pf_down * P.nsm;   // L2 prefetch about one wave ahead
+    if (ta < P.nmface) {
+      const int4 fn = P.fdesc[2 * P.mface[ta]];
+      const int mn = ((fn.z & 7) + 1) * (((fn.z >> 3) & 7) + 1);
+      l2_prefetch_span(P.qtrm + (long long)fn.x * NV, sizeof(double) * mn * NV);
+      l2_prefetch_span(P.qtrm + (long long)fn.y * NV, sizeof(double) * mn * NV);
+      l2_prefetch_span(P.face_geo + fn.w, sizeof(double) * mn * 4);
+      if (FLUX && L::viscous(P.prm)) {
+        l2_prefetch_span(P.gtrm + (long long)fn.x * NG, sizeof(double) * mn * NG);
+        l2_prefetch_span(P.gtrm + (long long)fn.y * NG, sizeof(double) * mn * NG);
+      }
     }
   }
-  const int4 tk = P.down[task];
-  const int M1 = tk.z & 7, M2 = (tk.z >> 3) & 7, o1 = (tk.z >> 6) & 7, o2 = (tk.z >> 9) & 7;
-  const int orient = (tk.z >> 12) & 7;
-  const bool right = (tk.z >> 15) & 1;
+  const int f = P.mface[task];
+  const int4 fd = P.fdesc[2 * f];
+  const int4 fo = P.fdesc[2 * f + 1];
+  const int M1 = fd.z & 7, M2 = (fd.z >> 3) & 7, orient = (fd.z >> 6) & 7;
   const int nm = (M1 + 1) * (M2 + 1);
-  const double* src = P.msurf + (long long)tk.x * C;
-  const double* T1 = P.tables + OFF_T + (M1 * 8 + o1) * 64;
-  const double* T2 = P.tables + OFF_T + (M2 * 8 + o2) * 64;
-  const int nf = (o1 + 1) * (o2 + 1);
-  double* out = dst + (long long)tk.y * C;
-  const auto ld = [&](int c, int a, int b) { return src[(long long)c * nm + a + (M1 + 1) * b]; };
-  if (!right)
-    warp_proj_mma<C>(M1 + 1, M2 + 1, T1, o1 + 1, T2, o2 + 1, ld,
-                     [&](int c, int A, int B, double x) { out[(long long)c * nf + A + (o1 + 1) * B] = x; });
-  else
-    warp_proj_mma<C>(M1 + 1, M2 + 1, T1, o1 + 1, T2, o2 + 1, ld,
-                     [&](int c, int A, int B, double x) {
-                       out[(long long)c * nf + right_index(A, B, o1, o2, orient)] = -x;
-                     });
+  const int g = lane >> 2, q = lane & 3;
+  const double* geo = P.face_geo + fd.w;
+  double v0[COUT], v1[COUT];
+#pragma unroll
+  for (int c = 0; c < COUT; ++c) v0[c] = v1[c] = 0.0;
+  if (g <= M2) {
+    if (q <= M1) {
+      const int t = q + (M1 + 1) * g;
+      face_point<LAW, FLUX>(P, P.qtrm, P.gtrm, fd.x, fd.y, nm, t, right_index(q, g, M1, M2, orient),
+                            geo, v0);
+    }
+    if (q + 4 <= M1) {
+      const int t = q + 4 + (M1 + 1) * g;
+      face_point<LAW, FLUX>(P, P.qtrm, P.gtrm, fd.x, fd.y, nm, t,
+                            right_index(q + 4, g, M1, M2, orient), geo, v1);
+    }
+  }
+  const auto ld = [&](int c, int a, int) { return a < 4 ? v0[c] : v1[c]; };
+  double* surf = FLUX ? P.fsurf : P.lsurf;
+  const int L1 = fo.w & 7, L2 = (fo.w >> 3) & 7, R1 = (fo.w >> 6) & 7, R2 = (fo.w >> 9) & 7;
+  {
+    double* out = surf + (long long)fo.y * COUT;
+    const int nf = (L1 + 1) * (L2 + 1);
+    warp_proj_mma<COUT>(M1 + 1, M2 + 1, P.tables + OFF_T + (M1 * 8 + L1) * 64, L1 + 1,
+                        P.tables + OFF_T + (M2 * 8 + L2) * 64, L2 + 1, ld,
+                        [&](int c, int A, int B, double x) { out[(long long)c * nf + A + (L1 + 1) * B] = x; });
+  }
+  {
+    double* out = surf + (long long)fo.z * COUT;
+    const int nf = (R1 + 1) * (R2 + 1);
+    warp_proj_mma<COUT>(M1 + 1, M2 + 1, P.tables + OFF_T + (M1 * 8 + R1) * 64, R1 + 1,
+                        P.tables + OFF_T + (M2 * 8 + R2) * 64, R2 + 1, ld,
+                        [&](int c, int A, int B, double x) {
+                          out[(long long)c * nf + right_index(A, B, R1, R2, orient)] = -x;
+                        });
+  }
 }
 
 // Side kernel: item = (slot, side, kind [-1 = isolated], ghost offset).
