@@ -130,7 +130,9 @@ __device__ __forceinline__ void block_max_to(double v, double* out, double* red 
 // FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col); per lane
 // a = A[lane/4][lane%4], b = B[lane%4][lane/4], d = D[lane/4][2(lane%4) + {0,1}].
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+  // not volatile: a pure function of its operands, so independent components'
+  // MMAs may be interleaved by the scheduler
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }

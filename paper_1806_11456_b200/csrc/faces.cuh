@@ -132,20 +132,6 @@ __global__ void __launch_bounds__(128, FLUX ? 4 : 5) k_mortar(DevPlan P) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int task = blockIdx.x * 4 + warp;
   if (task >= P.nmface) return;
-  if (lane == 0) {
-    const int ta = task + 4 * P.pf_down * P.nsm;   // L2 prefetch about one wave ahead
-    if (ta < P.nmface) {
-      const int4 fn = P.fdesc[2 * P.mface[ta]];
-      const int mn = ((fn.z & 7) + 1) * (((fn.z >> 3) & 7) + 1);
-      l2_prefetch_span(P.qtrm + (long long)fn.x * NV, sizeof(double) * mn * NV);
-      l2_prefetch_span(P.qtrm + (long long)fn.y * NV, sizeof(double) * mn * NV);
-      l2_prefetch_span(P.face_geo + fn.w, sizeof(double) * mn * 4);
-      if (FLUX && L::viscous(P.prm)) {
-        l2_prefetch_span(P.gtrm + (long long)fn.x * NG, sizeof(double) * mn * NG);
-        l2_prefetch_span(P.gtrm + (long long)fn.y * NG, sizeof(double) * mn * NG);
-      }
-    }
-  }
   const int f = P.mface[task];
   const int4 fd = P.fdesc[2 * f];
   const int4 fo = P.fdesc[2 * f + 1];
@@ -186,6 +172,22 @@ __global__ void __launch_bounds__(128, FLUX ? 4 : 5) k_mortar(DevPlan P) {
                         [&](int c, int A, int B, double x) {
                           out[(long long)c * nf + right_index(A, B, R1, R2, orient)] = -x;
                         });
+  }
+  // look-ahead L2 prefetch, issued after this warp's own work so that its
+  // dependent descriptor loads do not stall the projections
+  if (lane == 0) {
+    const int ta = task + 4 * P.pf_down * P.nsm;
+    if (ta < P.nmface) {
+      const int4 fn = P.fdesc[2 * P.mface[ta]];
+      const int mn = ((fn.z & 7) + 1) * (((fn.z >> 3) & 7) + 1);
+      l2_prefetch_span(P.qtrm + (long long)fn.x * NV, sizeof(double) * mn * NV);
+      l2_prefetch_span(P.qtrm + (long long)fn.y * NV, sizeof(double) * mn * NV);
+      l2_prefetch_span(P.face_geo + fn.w, sizeof(double) * mn * 4);
+      if (FLUX && L::viscous(P.prm)) {
+        l2_prefetch_span(P.gtrm + (long long)fn.x * NG, sizeof(double) * mn * NG);
+        l2_prefetch_span(P.gtrm + (long long)fn.y * NG, sizeof(double) * mn * NG);
+      }
+    }
   }
 }
 
