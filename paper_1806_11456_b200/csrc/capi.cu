@@ -138,6 +138,7 @@ struct tdg_plan {
   std::vector<int> orders_h;      // per slot
   std::vector<int> elem_id_h;
   std::vector<long long> node_off_h;
+  size_t smem_lift_own = 0;
   size_t smem_lift = 0, smem_flux = 0;
   int64_t side_nodes = 0;
   int iso = -1;          // isotropic order of a single-bucket plan, else -1
@@ -190,6 +191,7 @@ int setup_attrs(tdg_plan* p) {
     constexpr int NX = decltype(nx)::value;
     int r;
     if ((r = allow_smem(k_vol_lift<LAW, NX>, p->smem_lift))) return r;
+    if ((r = allow_smem(k_vol_lift_own<LAW, NX>, p->smem_lift_own))) return r;
     if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX>, p->smem_flux))) return r;
     if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX>, p->smem_flux))) return r;
     if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX>, p->smem_flux))) return r;
@@ -257,8 +259,13 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
     if ((rc = sides(false))) return rc;
     {
       KTimer kt(TDG_K_VOL_LIFT, st);
+      // LGL and every evaluated side on own-order traces: direct trace writes
+      const bool own = d.family == TDG_LGL && (isolated || d.nmface == 0);
       with_nx<LAW>(p->iso, [&](auto nx) -> int {
-        k_vol_lift<LAW, decltype(nx)::value><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q, coupled);
+        if (own)
+          k_vol_lift_own<LAW, decltype(nx)::value><<<d.nwork, ELEM_THREADS, p->smem_lift_own, st>>>(d, Q);
+        else
+          k_vol_lift<LAW, decltype(nx)::value><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q, coupled);
         return 0;
       });
     }
@@ -542,6 +549,11 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.fsurf = fsurf;
   d.grad = grad;
   p->smem_lift = static_cast<size_t>(std::max(p->ngv + 9, NG)) * MAXN * sizeof(double);
+  {
+    bool curved = false;
+    for (int s = 0; s < ns && !curved; ++s) curved = desc->affine[s] == 0;
+    p->smem_lift_own = static_cast<size_t>(p->ngv + (curved ? 9 : 0)) * MAXN * sizeof(double);
+  }
   p->smem_flux = static_cast<size_t>(3 * p->nv) * MAXN * sizeof(double);
   p->smem_flux_tma = static_cast<size_t>(p->nv == 5 ? tma_flux_smem_doubles<5, 12>()
                                                     : tma_flux_smem_doubles<1, 3>()) * sizeof(double);

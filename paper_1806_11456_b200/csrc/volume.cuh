@@ -160,6 +160,132 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
                            });
 }
 
+// BR1 lifted gradient at one node (operators.py:224-265): the volume part
+// −Σ_i WD_i(g Ja^i) from the staged g (and Ja on curved items), plus the
+// gathered surface contributions, times M⁻¹.  Shared by both lift kernels.
+template <int LAW, int NX>
+__device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T, const double* gs,
+                                          const double* js, bool aff, int tot, int n, int n1p,
+                                          int n2p, int n3p, int e, int node, int slot, int i, int j,
+                                          int k, double* out /* [3 NGV] */) {
+  using L = Law<LAW>;
+  constexpr int NGV = L::NGV, NG = 3 * NGV;
+  const int eb = e * n;
+  double acc[NG];
+#pragma unroll
+  for (int c = 0; c < NG; ++c) acc[c] = 0.0;
+  if (aff) {
+    // reference-space weak derivatives of g, then the constant metric transform
+    double W[3][NGV];
+#pragma unroll
+    for (int c = 0; c < 3 * NGV; ++c) W[c / NGV][c % NGV] = 0.0;
+    {
+      const double wo = T.w[1][j] * T.w[2][k];
+#pragma unroll
+      for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+        if (NX < 0 && m >= n1p) break;
+        const int idx = eb + m + n1p * (j + n2p * k);
+        const double dw = T.dh[0][m * 8 + i] * wo;
+#pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) W[0][kk] += dw * gs[kk * tot + idx];
+      }
+    }
+    {
+      const double wo = T.w[0][i] * T.w[2][k];
+#pragma unroll
+      for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+        if (NX < 0 && m >= n2p) break;
+        const int idx = eb + i + n1p * (m + n2p * k);
+        const double dw = T.dh[1][m * 8 + j] * wo;
+#pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) W[1][kk] += dw * gs[kk * tot + idx];
+      }
+    }
+    {
+      const double wo = T.w[0][i] * T.w[1][j];
+#pragma unroll
+      for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+        if (NX < 0 && m >= n3p) break;
+        const int idx = eb + i + n1p * (j + n2p * m);
+        const double dw = T.dh[2][m * 8 + k] * wo;
+#pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) W[2][kk] += dw * gs[kk * tot + idx];
+      }
+    }
+    const double* mj = P.metrics + P.metric_off[slot] + 1;   // Ja^i_d at [3 i + d]
+#pragma unroll
+    for (int ii = 0; ii < 3; ++ii) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double ja = mj[3 * ii + d];
+#pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * W[ii][kk];
+      }
+    }
+  } else {
+    {
+      const double wo = T.w[1][j] * T.w[2][k];
+      for (int m = 0; m < n1p; ++m) {
+        const int idx = eb + m + n1p * (j + n2p * k);
+        const double dw = T.dh[0][m * 8 + i] * wo;
+  #pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double ja = js[(0 * 3 + d) * tot + idx] * dw;
+  #pragma unroll
+          for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+        }
+      }
+    }
+    {
+      const double wo = T.w[0][i] * T.w[2][k];
+      for (int m = 0; m < n2p; ++m) {
+        const int idx = eb + i + n1p * (m + n2p * k);
+        const double dw = T.dh[1][m * 8 + j] * wo;
+  #pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double ja = js[(1 * 3 + d) * tot + idx] * dw;
+  #pragma unroll
+          for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+        }
+      }
+    }
+    {
+      const double wo = T.w[0][i] * T.w[1][j];
+      for (int m = 0; m < n3p; ++m) {
+        const int idx = eb + i + n1p * (j + n2p * m);
+        const double dw = T.dh[2][m * 8 + k] * wo;
+  #pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double ja = js[(2 * 3 + d) * tot + idx] * dw;
+  #pragma unroll
+          for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
+        }
+      }
+    }
+  }
+  // surface scatter of the lift contributions
+  const int ijk[3] = {i, j, k};
+  const int np[3] = {n1p, n2p, n3p};
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    int d, a, b;
+    side_dirs(s, d, a, b);
+    const double l = T.bnd[d][(s & 1) * 8 + ijk[d]];
+    if (l == 0.0) continue;
+    const int nf = np[a] * np[b];
+    const int kf = ijk[a] + np[a] * ijk[b];
+    const double lw = l * T.w[a][ijk[a]] * T.w[b][ijk[b]];
+    const double* src = P.lsurf + P.side_off[slot * 6 + s] * NG + kf;
+#pragma unroll
+    for (int c = 0; c < NG; ++c) acc[c] += lw * src[(long long)c * nf];
+  }
+  int ms;
+  const double* mp = metric_ptr(P, slot, node, n, ms);
+  const double invm = 1.0 / (T.w[0][i] * T.w[1][j] * T.w[2][k] * mp[0]);
+#pragma unroll
+  for (int c = 0; c < NG; ++c) out[c] = acc[c] * invm;
+}
+
 // ---------------------------------------------------------------------------
 // BR1 lift, volume part + scatter of the face contributions, times M^-1
 // (operators.py:224-265); writes the gradient and its side traces.
@@ -222,120 +348,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
     if (t < tot) {
       const int e = t / n, node = t - e * n, slot = wi.x + e;
       const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
-      const int eb = e * n;
-      double acc[NG];
-#pragma unroll
-      for (int c = 0; c < NG; ++c) acc[c] = 0.0;
-      if (aff) {
-        // reference-space weak derivatives of g, then the constant metric transform
-        double W[3][NGV];
-#pragma unroll
-        for (int c = 0; c < 3 * NGV; ++c) W[c / NGV][c % NGV] = 0.0;
-        {
-          const double wo = T.w[1][j] * T.w[2][k];
-#pragma unroll
-          for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
-            if (NX < 0 && m >= n1p) break;
-            const int idx = eb + m + n1p * (j + n2p * k);
-            const double dw = T.dh[0][m * 8 + i] * wo;
-#pragma unroll
-            for (int kk = 0; kk < NGV; ++kk) W[0][kk] += dw * gs[kk * tot + idx];
-          }
-        }
-        {
-          const double wo = T.w[0][i] * T.w[2][k];
-#pragma unroll
-          for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
-            if (NX < 0 && m >= n2p) break;
-            const int idx = eb + i + n1p * (m + n2p * k);
-            const double dw = T.dh[1][m * 8 + j] * wo;
-#pragma unroll
-            for (int kk = 0; kk < NGV; ++kk) W[1][kk] += dw * gs[kk * tot + idx];
-          }
-        }
-        {
-          const double wo = T.w[0][i] * T.w[1][j];
-#pragma unroll
-          for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
-            if (NX < 0 && m >= n3p) break;
-            const int idx = eb + i + n1p * (j + n2p * m);
-            const double dw = T.dh[2][m * 8 + k] * wo;
-#pragma unroll
-            for (int kk = 0; kk < NGV; ++kk) W[2][kk] += dw * gs[kk * tot + idx];
-          }
-        }
-        const double* mj = P.metrics + P.metric_off[slot] + 1;   // Ja^i_d at [3 i + d]
-#pragma unroll
-        for (int ii = 0; ii < 3; ++ii) {
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const double ja = mj[3 * ii + d];
-#pragma unroll
-            for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * W[ii][kk];
-          }
-        }
-      } else {
-        {
-          const double wo = T.w[1][j] * T.w[2][k];
-          for (int m = 0; m < n1p; ++m) {
-            const int idx = eb + m + n1p * (j + n2p * k);
-            const double dw = T.dh[0][m * 8 + i] * wo;
-  #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              const double ja = js[(0 * 3 + d) * tot + idx] * dw;
-  #pragma unroll
-              for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
-            }
-          }
-        }
-        {
-          const double wo = T.w[0][i] * T.w[2][k];
-          for (int m = 0; m < n2p; ++m) {
-            const int idx = eb + i + n1p * (m + n2p * k);
-            const double dw = T.dh[1][m * 8 + j] * wo;
-  #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              const double ja = js[(1 * 3 + d) * tot + idx] * dw;
-  #pragma unroll
-              for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
-            }
-          }
-        }
-        {
-          const double wo = T.w[0][i] * T.w[1][j];
-          for (int m = 0; m < n3p; ++m) {
-            const int idx = eb + i + n1p * (j + n2p * m);
-            const double dw = T.dh[2][m * 8 + k] * wo;
-  #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              const double ja = js[(2 * 3 + d) * tot + idx] * dw;
-  #pragma unroll
-              for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * gs[kk * tot + idx];
-            }
-          }
-        }
-      }
-      // surface scatter of the lift contributions
-      const int ijk[3] = {i, j, k};
-      const int np[3] = {n1p, n2p, n3p};
-#pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        int d, a, b;
-        side_dirs(s, d, a, b);
-        const double l = T.bnd[d][(s & 1) * 8 + ijk[d]];
-        if (l == 0.0) continue;
-        const int nf = np[a] * np[b];
-        const int kf = ijk[a] + np[a] * ijk[b];
-        const double lw = l * T.w[a][ijk[a]] * T.w[b][ijk[b]];
-        const double* src = P.lsurf + P.side_off[slot * 6 + s] * NG + kf;
-#pragma unroll
-        for (int c = 0; c < NG; ++c) acc[c] += lw * src[(long long)c * nf];
-      }
-      int ms;
-      const double* mp = metric_ptr(P, slot, node, n, ms);
-      const double invm = 1.0 / (T.w[0][i] * T.w[1][j] * T.w[2][k] * mp[0]);
-#pragma unroll
-      for (int c = 0; c < NG; ++c) Greg[r][c] = acc[c] * invm;
+      lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, Greg[r]);
     }
   }
   __syncthreads();
@@ -361,6 +374,83 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
     const int strides[3] = {1, n1p, n1p * n2p};
     item_side_traces<NG>(P, wi.x, wi.y, coupled, np, strides, T.bnd, P.gtr, P.gtrm,
                          [&](int e, int c, int off) { return G[c * tot + e * n + off]; });
+  }
+}
+
+// BR1 lift for LGL plans whose evaluated sides all use own-order traces (no
+// nonconforming face, or an isolated evaluation): the side traces of G are
+// face-node values, so every node writes its gradient straight to ``grad``
+// and to the own-order trace arrays of the sides it lies on.  No staging of
+// G in shared memory and no second barrier, so each thread keeps one node's
+// values at a time: 64 registers, 4 blocks per SM.
+template <int LAW, int NX>
+__global__ void __launch_bounds__(ELEM_THREADS, 4) k_vol_lift_own(DevPlan P, const double* __restrict__ Q) {
+  using L = Law<LAW>;
+  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
+  __shared__ ElemTables T;
+  __shared__ int s_aff;
+  extern __shared__ double sm[];
+  const int2 wi = P.work[blockIdx.x];
+  const int* od = P.orders + 3 * wi.x;
+  const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
+  prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+  load_tables(P, N1, N2, N3, T);
+  if (threadIdx.x == 0) {
+    int a = 1;
+    for (int e = 0; e < wi.y; ++e) a &= P.affine[wi.x + e] != 0;
+    s_aff = a;
+  }
+  const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
+  const int n = n1p * n2p * n3p, tot = wi.y * n;
+  double* gs = sm;               // [NGV][tot]
+  double* js = sm + NGV * tot;   // [9][tot]  (curved items only)
+  __syncthreads();
+  const bool aff = s_aff != 0;
+#pragma unroll 1
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * ELEM_THREADS;
+    if (t < tot) {
+      const int e = t / n, node = t - e * n, slot = wi.x + e;
+      const long long base = P.node_off[slot] * NV;
+      double q[NV], g[NGV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) q[v] = Q[base + (long long)v * n + node];
+      L::grad_vars(P.prm, q, g);
+#pragma unroll
+      for (int k = 0; k < NGV; ++k) gs[k * tot + t] = g[k];
+      if (!aff) {
+        int ms;
+        const double* m = metric_ptr(P, slot, node, n, ms);
+#pragma unroll
+        for (int c = 0; c < 9; ++c) js[c * tot + t] = m[(1 + c) * ms];
+      }
+    }
+  }
+  __syncthreads();
+  const int np[3] = {n1p, n2p, n3p};
+#pragma unroll 1
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * ELEM_THREADS;
+    if (t < tot) {
+      const int e = t / n, node = t - e * n, slot = wi.x + e;
+      const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+      double x[NG];
+      lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+      const long long gb = P.node_off[slot] * NG;
+#pragma unroll
+      for (int c = 0; c < NG; ++c) P.grad[gb + (long long)c * n + node] = x[c];
+      const int ijk[3] = {i, j, k};
+#pragma unroll
+      for (int s = 0; s < 6; ++s) {
+        int d, a, b;
+        side_dirs(s, d, a, b);
+        if (ijk[d] != ((s & 1) ? np[d] - 1 : 0)) continue;
+        const int nf = np[a] * np[b];
+        double* dst = P.gtr + P.side_off[slot * 6 + s] * NG + ijk[a] + np[a] * ijk[b];
+#pragma unroll
+        for (int c = 0; c < NG; ++c) dst[(long long)c * nf] = x[c];
+      }
+    }
   }
 }
 
