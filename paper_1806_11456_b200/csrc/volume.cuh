@@ -382,9 +382,10 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
 // face-node values, so every node writes its gradient straight to ``grad``
 // and to the own-order trace arrays of the sides it lies on.  No staging of
 // G in shared memory and no second barrier, so each thread keeps one node's
-// values at a time: 64 registers, 4 blocks per SM.
+// values at a time (80 registers without spills, 3 blocks per SM: measured
+// faster than 4 blocks with spills at 64).
 template <int LAW, int NX>
-__global__ void __launch_bounds__(ELEM_THREADS, 4) k_vol_lift_own(DevPlan P, const double* __restrict__ Q) {
+__global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, const double* __restrict__ Q) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
