@@ -151,6 +151,17 @@ int tdg_rk3_stage(tdg_plan* plan, double* Q, double* W, const double* S, int sta
                   const double* dt, int local, double* rnorm_dev, int32_t* nonfinite_dev,
                   void* stream);
 
+/* tdg_rk3_stage with flags.  TDG_RK_TRACES_FRESH: the caller guarantees that
+   Q has not been modified since the previous evaluation on this plan (the
+   next stage of an RK step, or the next sweep of a smoothing run).  On LGL
+   plans without nonconforming faces every RK stage writes the own-order side
+   traces of its new state in its epilogue, and a fresh stage then skips the
+   trace pass.  Results are identical with or without the flag. */
+#define TDG_RK_TRACES_FRESH 1
+int tdg_rk3_stage_ex(tdg_plan* plan, double* Q, double* W, const double* S, int stage,
+                     const double* dt, int local, double* rnorm, int32_t* nonfinite, int flags,
+                     void* stream);
+
 /* NodalField.norm_inf / element_norms_inf (fields.py:144-152):
  * max_dev (nullable) = max|X| (reset inside); elem_dev (nullable, by element id). */
 int tdg_norm_inf(tdg_plan* plan, const double* X, double* max_dev, double* elem_dev,

@@ -11,6 +11,7 @@ import os
 from .errors import ConfigError, DeviceError, MeshError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
+RK_TRACES_FRESH = 1   # include/taudg.h TDG_RK_TRACES_FRESH
 # TDG_LIB_PATH: development override (A/B builds of the same C-ABI)
 LIB_PATH = os.environ.get("TDG_LIB_PATH") or os.path.join(_HERE, "_taudg.so")
 
@@ -54,6 +55,7 @@ SIGNATURES = {
     "tdg_tau": ([_VP, _VP, _VP, _VP, C.c_int, _VP], C.c_int),
     "tdg_element_dt": ([_VP, _VP, _dbl, _dbl, _VP, _VP, _VP], C.c_int),
     "tdg_rk3_stage": ([_VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, _VP, _VP, _VP], C.c_int),
+    "tdg_rk3_stage_ex": ([_VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, _VP, _VP, C.c_int, _VP], C.c_int),
     "tdg_norm_inf": ([_VP, _VP, _VP, _VP, _VP], C.c_int),
     "tdg_check_finite": ([_VP, _VP, _VP, _VP], C.c_int),
     "tdg_transfer_create": ([C.POINTER(TransferDesc), C.POINTER(_VP)], C.c_int),

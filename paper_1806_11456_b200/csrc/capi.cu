@@ -139,6 +139,11 @@ struct tdg_plan {
   std::vector<int> elem_id_h;
   std::vector<long long> node_off_h;
   size_t smem_lift_own = 0;
+  // Q buffer whose current contents the own-order trace array qtr holds
+  // (set by evaluations; an RK stage leaves the traces of its new state only
+  // when its epilogue wrote them)
+  const double* traces_of = nullptr;
+  bool rk_traces = false;   // LGL, no nonconforming face, no TMA kernel
   size_t smem_lift = 0, smem_flux = 0;
   int64_t side_nodes = 0;
   int iso = -1;          // isotropic order of a single-bucket plan, else -1
@@ -212,13 +217,17 @@ int setup_attrs(tdg_plan* p) {
 
 // trace -> lift (if viscous) -> face fluxes; leaves fsurf ready for k_vol_flux
 template <int LAW>
-int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
+int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st, bool traces_fresh = false) {
   using L = Law<LAW>;
   const DevPlan& d = p->d;
   if (d.nwork == 0) return TDG_OK;
   const int coupled = isolated ? 0 : 1;
-  { KTimer kt(TDG_K_TRACE, st); k_trace_q<L::NV><<<d.nwork, ELEM_THREADS, 0, st>>>(d, Q, coupled); }
-  LAUNCH_CHECK("k_trace_q");
+  if (!traces_fresh) {
+    KTimer kt(TDG_K_TRACE, st);
+    k_trace_q<L::NV><<<d.nwork, ELEM_THREADS, 0, st>>>(d, Q, coupled);
+    LAUNCH_CHECK("k_trace_q");
+  }
+  p->traces_of = Q;
 
   auto sides = [&](bool flux) -> int {
     const int4* items = isolated ? d.side_iso : d.side_bnd;
@@ -275,8 +284,9 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st) {
 }
 
 template <int LAW, int MODE>
-int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cudaStream_t st) {
-  int rc = run_surface<LAW>(p, Q, isolated, st);
+int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cudaStream_t st,
+             bool traces_fresh = false) {
+  int rc = run_surface<LAW>(p, Q, isolated, st, traces_fresh);
   if (rc) return rc;
   if (p->d.nwork == 0) return TDG_OK;
   {
@@ -295,15 +305,18 @@ int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cuda
     }
   }
   LAUNCH_CHECK("k_vol_flux");
+  // an RK stage rewrote Q: qtr now holds its traces only if the epilogue wrote them
+  if (MODE == MODE_RK) p->traces_of = a.traces ? Q : nullptr;
   return TDG_OK;
 }
 
 template <int MODE>
-int dispatch_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cudaStream_t st) {
+int dispatch_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cudaStream_t st,
+                  bool traces_fresh = false) {
   switch (p->d.law) {
-    case TDG_LAW_ADVDIFF: return run_eval<LAW_ADVDIFF, MODE>(p, Q, isolated, a, st);
-    case TDG_LAW_BURGERS: return run_eval<LAW_BURGERS, MODE>(p, Q, isolated, a, st);
-    case TDG_LAW_NS: return run_eval<LAW_NS, MODE>(p, Q, isolated, a, st);
+    case TDG_LAW_ADVDIFF: return run_eval<LAW_ADVDIFF, MODE>(p, Q, isolated, a, st, traces_fresh);
+    case TDG_LAW_BURGERS: return run_eval<LAW_BURGERS, MODE>(p, Q, isolated, a, st, traces_fresh);
+    case TDG_LAW_NS: return run_eval<LAW_NS, MODE>(p, Q, isolated, a, st, traces_fresh);
   }
   return fail(TDG_E_CONFIG, "unknown law");
 }
@@ -562,6 +575,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     // (compute-phase latency dominates once loads are decoupled); opt-in
     const char* env = getenv("TDG_TMA");
     p->tma = env && env[0] == '1';
+    p->rk_traces = desc->family == TDG_LGL && d.nmface == 0 && !p->tma;
     int dev = 0, nsm = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
@@ -633,6 +647,11 @@ int tdg_tau(tdg_plan* p, const double* Q, const double* S, double* tau, int isol
 
 int tdg_rk3_stage(tdg_plan* p, double* Q, double* W, const double* S, int stage, const double* dt,
                   int local, double* rnorm, int32_t* nonfinite, void* stream) {
+  return tdg_rk3_stage_ex(p, Q, W, S, stage, dt, local, rnorm, nonfinite, 0, stream);
+}
+
+int tdg_rk3_stage_ex(tdg_plan* p, double* Q, double* W, const double* S, int stage, const double* dt,
+                     int local, double* rnorm, int32_t* nonfinite, int flags, void* stream) {
   static const double RK_A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};   // timestep.py:18-20
   static const double RK_B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
   if (!p || !Q || !W || !dt) return fail(TDG_E_ARG, "null argument");
@@ -648,7 +667,11 @@ int tdg_rk3_stage(tdg_plan* p, double* Q, double* W, const double* S, int stage,
   a.rk_b = RK_B[stage];
   a.norm = rnorm;
   a.nonfinite = reinterpret_cast<int*>(nonfinite);
-  return dispatch_eval<MODE_RK>(p, Q, 0, a, as_stream(stream));
+  a.traces = p->rk_traces ? 1 : 0;
+  // the caller vouches that Q is unchanged since the previous call on this
+  // plan; the traces are reused if that call left them for this buffer
+  const bool fresh = (flags & TDG_RK_TRACES_FRESH) && p->rk_traces && p->traces_of == Q;
+  return dispatch_eval<MODE_RK>(p, Q, 0, a, as_stream(stream), fresh);
 }
 
 int tdg_element_dt(tdg_plan* p, const double* Q, double cfl_a, double cfl_v, double* dt_slot,

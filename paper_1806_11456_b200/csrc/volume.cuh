@@ -470,6 +470,7 @@ struct FluxArgs {
   double rk_a, rk_b;
   double* norm;        // max |r|
   int* nonfinite;
+  int traces;          // RK: also write the new state's own-order Q traces (LGL, conforming)
 };
 
 template <int LAW, int MODE, int NX>
@@ -614,6 +615,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
       } else if (MODE == MODE_RK) {
         const double dtv = A.local ? A.dt[slot] : A.dt[0];
         bool bad = false;
+        double qn[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           const long long ix = base + (long long)v * n;
@@ -622,11 +624,26 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
           rmax = nanmax(rmax, fabs(rv));
           const double wv = (A.stage == 0) ? rv : A.rk_a * A.W[ix] + rv;
           A.W[ix] = wv;
-          const double qn = A.Qout[ix] + A.rk_b * dtv * wv;
-          A.Qout[ix] = qn;
-          bad |= !isfinite(qn);
+          qn[v] = A.Qout[ix] + A.rk_b * dtv * wv;
+          A.Qout[ix] = qn[v];
+          bad |= !isfinite(qn[v]);
         }
         if (bad && A.nonfinite) *A.nonfinite = 1;
+        if (A.traces) {
+          // LGL face nodes: the next stage's own-order Q traces (k_trace_q skipped)
+          const int ijk[3] = {i, j, k};
+          const int np[3] = {n1p, n2p, n3p};
+#pragma unroll 1
+          for (int sd = 0; sd < 6; ++sd) {
+            int d, a, b;
+            side_dirs(sd, d, a, b);
+            if (ijk[d] != ((sd & 1) ? np[d] - 1 : 0)) continue;
+            const int nf = np[a] * np[b];
+            double* dst = P.qtr + P.side_off[slot * 6 + sd] * NV + ijk[a] + np[a] * ijk[b];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) dst[(long long)v * nf] = qn[v];
+          }
+        }
       } else if (MODE == MODE_TAU) {
         double tv = 0.0;
 #pragma unroll

@@ -530,7 +530,11 @@ class DGOperator:
         _lib.call("tdg_element_dt", self._plan, _lib.ptr(Q.data), float(cfl_adv), float(cfl_visc),
                   _lib.ptr(dt_slot), _lib.ptr(dt_min), self._stream())
 
-    def rk3_stage(self, Q, W, S, stage, dt, local, rnorm=None, nonfinite=None):
-        _lib.call("tdg_rk3_stage", self._plan, _lib.ptr(Q.data), _lib.ptr(W.data),
+    def rk3_stage(self, Q, W, S, stage, dt, local, rnorm=None, nonfinite=None, fresh=False):
+        """One fused RK3 stage.  ``fresh``: Q is unchanged since the previous
+        evaluation on this operator (the next stage or sweep of a smoothing
+        run), so the library may reuse the side traces that stage left."""
+        _lib.call("tdg_rk3_stage_ex", self._plan, _lib.ptr(Q.data), _lib.ptr(W.data),
                   _lib.ptr(S.data if S is not None else None), int(stage), _lib.ptr(dt), int(bool(local)),
-                  _lib.ptr(rnorm), _lib.ptr(nonfinite), self._stream())
+                  _lib.ptr(rnorm), _lib.ptr(nonfinite), _lib.RK_TRACES_FRESH if fresh else 0,
+                  self._stream())

@@ -90,11 +90,12 @@ def _device_dt(op, Q, config, s):
 
 
 def rk3_step(op, Q: NodalField, dt, source: NodalField | None = None,
-             work: NodalField | None = None, rnorm=None, nonfinite=None):
+             work: NodalField | None = None, rnorm=None, nonfinite=None, fresh=False):
     """One RK3 step; ``dt`` is a float, a per-element numpy array (by element
     id) or a device tensor (scalar or per slot).  Returns the stage-0 residual
     inf-norm as a float when ``rnorm`` is None (reference semantics), else
-    leaves it in the device scalar ``rnorm``."""
+    leaves it in the device scalar ``rnorm``.  ``fresh``: Q is unchanged since
+    the previous RK stage on ``op`` (later stages always are)."""
     import torch
 
     s = _scratch(op)
@@ -114,7 +115,8 @@ def rk3_step(op, Q: NodalField, dt, source: NodalField | None = None,
         rnorm = torch.zeros(1, dtype=torch.float64, device=op.device)
     for stage in range(3):
         op.calls["apply"] += 1
-        op.rk3_stage(Q, work, src, stage, dt_dev, local, rnorm=rnorm, nonfinite=nonfinite)
+        op.rk3_stage(Q, work, src, stage, dt_dev, local, rnorm=rnorm, nonfinite=nonfinite,
+                     fresh=fresh or stage > 0)
     return float(rnorm.item()) if sync else rnorm
 
 
@@ -138,7 +140,8 @@ def smooth(op, Q: NodalField, sweeps: int, config: TimeConfig, source: NodalFiel
     for k in range(sweeps):
         dt = _device_dt(op, Q, config, s)
         dts[k: k + 1].copy_(s.dt_min)
-        rk3_step(op, Q, dt, source=source, work=s.work, rnorm=norms[k: k + 1], nonfinite=flags[k: k + 1])
+        rk3_step(op, Q, dt, source=source, work=s.work, rnorm=norms[k: k + 1], nonfinite=flags[k: k + 1],
+                 fresh=k > 0)
     h_norms = norms.cpu().numpy()
     h_dts = dts.cpu().numpy()
     h_flags = flags.cpu().numpy()

@@ -135,3 +135,40 @@ def test_ns_vcycle_and_tau_match_oracle():
             assert set(tm.tau[e][d]) == set(tmo.tau[e][d])
             for n, v in tmo.tau[e][d].items():
                 assert abs(tm.tau[e][d][n] - v) <= 1e-12 * scale
+
+
+def test_rk_stage_trace_reuse_is_bitwise_identical():
+    """TDG_RK_TRACES_FRESH (include/taudg.h): on an LGL plan without
+    nonconforming faces the RK epilogue leaves the next stage's side traces and
+    the fresh stage skips the trace pass; the states must match bit for bit the
+    run that recomputes every trace (and a foreign buffer must not reuse them)."""
+    import torch
+
+    from paper_1806_11456_b200 import configs, operators, timestep
+
+    w = configs.config1()
+    op = operators.DGOperator(w.mesh, w.law, w.orders, family=w.family, form=w.form)
+    Q0 = op.project_function(w.init)
+    dt = 1e-3
+    runs = []
+    for fresh in (False, True):
+        Q = Q0.copy()
+        W = Q0.copy()
+        for sweep in range(3):
+            for stage in range(3):
+                op.rk3_stage(Q, W, op.source, stage,
+                             torch.full((1,), dt, dtype=torch.float64, device="cuda"), False,
+                             fresh=fresh and (sweep > 0 or stage > 0))
+        runs.append(Q.data.clone())
+    assert torch.equal(runs[0], runs[1])
+    # a fresh stage on another buffer must not pick up the first buffer's traces
+    Qa, Qb = Q0.copy(), Q0.copy()
+    Qb.data.mul_(1.001)
+    W = Q0.copy()
+    dt_t = torch.full((1,), dt, dtype=torch.float64, device="cuda")
+    op.rk3_stage(Qa, W, op.source, 0, dt_t, False)
+    ref = Qb.copy()
+    Wr = Q0.copy()
+    op.rk3_stage(ref, Wr, op.source, 0, dt_t, False)
+    op.rk3_stage(Qb, W, op.source, 0, dt_t, False, fresh=True)
+    assert torch.equal(Qb.data, ref.data)
