@@ -158,6 +158,7 @@ struct tdg_transfer {
   int nwork = 0;
   size_t smem = 0;
   int nv = 1;
+  int iso_f = 0, iso_c = 0;   // points per direction when every element is isotropic and uniform
 };
 
 namespace {
@@ -322,6 +323,40 @@ int dispatch_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a,
 }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Transfer launch: compile-time sizes for the isotropic neighbour-order level
+// pairs of a uniform p-multigrid (5 components), runtime sizes otherwise.
+template <int MODE, int NS, int ND>
+bool launch_transfer_iso(const tdg_transfer* t, int ns, int nd, const double* in, const double* in2,
+                         double* out, cudaStream_t st) {
+  if (ns != NS || nd != ND) return false;
+  k_transfer<MODE, 5, NS, ND><<<t->nwork, ELEM_THREADS, t->smem, st>>>(t->d, in, in2, out);
+  return true;
+}
+
+template <int MODE>
+int launch_transfer(const tdg_transfer* t, const double* in, const double* in2, double* out,
+                    cudaStream_t st) {
+  const int ns = MODE == TR_RESTRICT ? t->iso_f : t->iso_c;
+  const int nd = MODE == TR_RESTRICT ? t->iso_c : t->iso_f;
+  bool done = false;
+  if (t->nv == 5 && ns > 0 && nd > 0) {
+    done = launch_transfer_iso<MODE, 8, 7>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 7, 8>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 7, 6>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 6, 7>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 6, 5>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 5, 6>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 5, 4>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 4, 5>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 4, 3>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 3, 4>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 3, 2>(t, ns, nd, in, in2, out, st) ||
+           launch_transfer_iso<MODE, 2, 3>(t, ns, nd, in, in2, out, st);
+  }
+  if (!done) k_transfer<MODE><<<t->nwork, ELEM_THREADS, t->smem, st>>>(t->d, in, in2, out);
+  return TDG_OK;
+}
 
 }  // namespace
 
@@ -823,6 +858,16 @@ int tdg_transfer_create(const tdg_transfer_desc* desc, tdg_transfer** out) {
   t->d.work = work_d;
   t->nwork = static_cast<int>(work.size());
   t->smem = 2 * static_cast<size_t>(t->nv) * MAXN * sizeof(double);
+  {
+    auto iso_points = [](const std::vector<int>& o, int n) {
+      if (n == 0) return 0;
+      for (int k = 0; k < 3 * n; ++k)
+        if (o[k] != o[0]) return 0;
+      return o[0] + 1;
+    };
+    t->iso_f = iso_points(f_orders, ns);
+    t->iso_c = iso_points(c_orders, static_cast<int>(c_orders.size() / 3));
+  }
   if ((rc = allow_smem(k_transfer<TR_RESTRICT>, t->smem)) || (rc = allow_smem(k_transfer<TR_PROLONG>, t->smem)) ||
       (rc = allow_smem(k_transfer<TR_PROLONG_ADD>, t->smem))) {
     delete t;
@@ -841,7 +886,7 @@ int tdg_restrict(const tdg_transfer* t, const double* fine, double* coarse, void
   if (!t || !fine || !coarse) return fail(TDG_E_ARG, "null argument");
   if (!t->nwork) return TDG_OK;
   KTimer kt(TDG_K_TRANSFER, as_stream(stream));
-  k_transfer<TR_RESTRICT><<<t->nwork, ELEM_THREADS, t->smem, as_stream(stream)>>>(t->d, fine, nullptr, coarse);
+  launch_transfer<TR_RESTRICT>(t, fine, nullptr, coarse, as_stream(stream));
   LAUNCH_CHECK("k_transfer(restrict)");
   return TDG_OK;
 }
@@ -850,7 +895,7 @@ int tdg_prolong(const tdg_transfer* t, const double* coarse, double* fine, void*
   if (!t || !fine || !coarse) return fail(TDG_E_ARG, "null argument");
   if (!t->nwork) return TDG_OK;
   KTimer kt(TDG_K_TRANSFER, as_stream(stream));
-  k_transfer<TR_PROLONG><<<t->nwork, ELEM_THREADS, t->smem, as_stream(stream)>>>(t->d, coarse, nullptr, fine);
+  launch_transfer<TR_PROLONG>(t, coarse, nullptr, fine, as_stream(stream));
   LAUNCH_CHECK("k_transfer(prolong)");
   return TDG_OK;
 }
@@ -860,7 +905,7 @@ int tdg_prolong_add(const tdg_transfer* t, const double* Qc, const double* Qc0, 
   if (!t || !fine || !Qc) return fail(TDG_E_ARG, "null argument");
   if (!t->nwork) return TDG_OK;
   KTimer kt(TDG_K_TRANSFER, as_stream(stream));
-  k_transfer<TR_PROLONG_ADD><<<t->nwork, ELEM_THREADS, t->smem, as_stream(stream)>>>(t->d, Qc, Qc0, fine);
+  launch_transfer<TR_PROLONG_ADD>(t, Qc, Qc0, fine, as_stream(stream));
   LAUNCH_CHECK("k_transfer(prolong_add)");
   return TDG_OK;
 }

@@ -23,7 +23,11 @@ struct DevTransfer {
   const int2* work;         // (first fine slot, count)
 };
 
-template <int MODE>
+// NVC > 0, NSC > 0, NDC > 0: compile-time component count and isotropic
+// source / target point counts (the uniform p-multigrid level pairs), so the
+// index arithmetic of every pass folds to constant divisors; otherwise all
+// runtime.
+template <int MODE, int NVC = -1, int NSC = -1, int NDC = -1>
 __global__ void __launch_bounds__(ELEM_THREADS) k_transfer(DevTransfer T, const double* __restrict__ in,
                                                            const double* __restrict__ in2,
                                                            double* __restrict__ out) {
@@ -38,14 +42,14 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_transfer(DevTransfer T, const 
   int sn[3], dn[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
-    sn[d] = (down ? fo[d] : co[d]) + 1;
-    dn[d] = (down ? co[d] : fo[d]) + 1;
+    sn[d] = NSC > 0 ? NSC : (down ? fo[d] : co[d]) + 1;
+    dn[d] = NDC > 0 ? NDC : (down ? co[d] : fo[d]) + 1;
   }
   for (int u = threadIdx.x; u < 3 * 64; u += blockDim.x) {
     const int d = u / 64;
     mat[d][u % 64] = T.tables[OFF_T + ((sn[d] - 1) * 8 + (dn[d] - 1)) * 64 + (u % 64)];
   }
-  const int nv = T.nv;
+  const int nv = NVC > 0 ? NVC : T.nv;
   const int ns = sn[0] * sn[1] * sn[2], nd = dn[0] * dn[1] * dn[2];
   const int s1 = dn[0] * sn[1] * sn[2], s2 = dn[0] * dn[1] * sn[2];
   int mx = ns > nd ? ns : nd;
