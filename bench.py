@@ -272,33 +272,33 @@ def run_b200(args):
                 "kernel_ms_per_step": {k: round(v / args.steps, 4) for k, v in shares.items()}}
 
     # ---- end to end through the public API with host buffers -------------------
-    Qh = Q.data.cpu().pin_memory()
-    Rh = torch.empty_like(Qh).pin_memory()
-    nh = torch.empty(1, dtype=torch.float64).pin_memory()
-    Qd = op.new_field()
-
-    def e2e_step():
-        Qd.data.copy_(Qh, non_blocking=True)
-        op.residual_device(Qd, None, out=R, norm=norm)
-        Rh.copy_(R.data, non_blocking=True)
-        nh.copy_(norm, non_blocking=True)
-
-    for _ in range(2):
-        e2e_step()
+    # Page-locked host states (4 distinct buffers, cycled) evaluated by the
+    # host-buffer batch call: every one of the K steps copies its state in and
+    # its residual and max|r| out, the copies of neighbouring steps overlapping
+    # the evaluation (tdg_residual_host)
+    q0 = Q.data.cpu()
+    nbuf = min(4, args.steps)
+    bufs = [q0.clone().pin_memory() for _ in range(nbuf)]
+    for k, q in enumerate(bufs):
+        q[k] += 1e-12 * k        # distinct states
+    outs = [torch.empty_like(q0).pin_memory() for _ in range(nbuf)]
+    Qh = [bufs[k % nbuf] for k in range(args.steps)]
+    Rh = [outs[k % nbuf] for k in range(args.steps)]
+    op.residual_host(Qh[:2], out=Rh[:2])
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
+    _, host_norms = op.residual_host(Qh, out=Rh)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
     e_ms = max_over_ranks(e0.elapsed_time(e1))
     e2e = {"value": nodes * args.steps * ws / (e_ms / 1000.0), "unit": "DOF-evals/s",
-           "h2d_bytes_per_step": Qh.numel() * 8, "d2h_bytes_per_step": Rh.numel() * 8 + 8,
-           "ms_per_step": e_ms / args.steps}
-    del op, Q, R, Qd
+           "h2d_bytes_per_step": q0.numel() * 8, "d2h_bytes_per_step": q0.numel() * 8 + 8,
+           "ms_per_step": e_ms / args.steps, "api": "DGOperator.residual_host (tdg_residual_host)",
+           "overlap": "double-buffered: H2D of step k+1 and D2H of step k-1 overlap step k"}
+    del op, Q, R, Qh, Rh, bufs, outs
 
     # ---- V-cycle, config 4 --------------------------------------------------------
     vcycle = None

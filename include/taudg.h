@@ -129,6 +129,20 @@ int tdg_m_inv_apply(tdg_plan* plan, const double* Q, const double* add, double* 
 int tdg_residual(tdg_plan* plan, const double* Q, const double* S, double* R,
                  double* rnorm_dev, void* stream);
 
+/* DGOperator.residual (operators.py:344-353) on HOST buffers, for a batch of
+ * independent states: R_host[b] = S - F(Q_host[b])/M, rnorm_host[b] = max|R|.
+ * The reference's residual takes and returns host arrays; this is that call
+ * for nbatch states at once.  Each state is copied in, evaluated and copied
+ * out through two plan-owned device staging slots on two copy streams, so the
+ * host->device copy of state b+1 and the device->host copy of state b-1 overlap
+ * the evaluation of state b (use page-locked host buffers for the overlap).
+ * S_dev is a device field (nullable, zero) shared by the batch; rnorm_host is
+ * nullable.  Ordered after prior work on `stream`; returns when every R_host
+ * and rnorm_host entry is written, with `stream` ordered after the copies. */
+int tdg_residual_host(tdg_plan* plan, int32_t nbatch, const double* const* Q_host,
+                      const double* S_dev, double* const* R_host, double* rnorm_host,
+                      void* stream);
+
 /* DGOperator.truncation / truncation_from_avalue (operators.py:355-364) and
  * tau.recorder_for (tau.py:173-183): tau[elem_id] = max |M S_pde - F(Q)|
  * over nodes and unknowns, with F isolated or coupled.  tau_dev has

@@ -52,6 +52,7 @@ SIGNATURES = {
     "tdg_apply": ([_VP, _VP, _VP, C.c_int, _VP], C.c_int),
     "tdg_m_inv_apply": ([_VP, _VP, _VP, _VP, C.c_int, _VP], C.c_int),
     "tdg_residual": ([_VP, _VP, _VP, _VP, _VP, _VP], C.c_int),
+    "tdg_residual_host": ([_VP, _i32, C.POINTER(_VP), _VP, C.POINTER(_VP), _pd, _VP], C.c_int),
     "tdg_tau": ([_VP, _VP, _VP, _VP, C.c_int, _VP], C.c_int),
     "tdg_element_dt": ([_VP, _VP, _dbl, _dbl, _VP, _VP, _VP], C.c_int),
     "tdg_rk3_stage": ([_VP, _VP, _VP, _VP, C.c_int, _VP, C.c_int, _VP, _VP, _VP], C.c_int),

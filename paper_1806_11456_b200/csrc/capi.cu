@@ -150,6 +150,37 @@ struct tdg_plan {
   bool tma = false;      // persistent TMA-pipelined flux kernel (TDG_TMA=1 enables)
   int nsm = 148;
   size_t smem_flux_tma = 0;
+  // host-buffer batch evaluation (tdg_residual_host): two device staging
+  // slots, two copy streams, per-slot events; created on first use
+  struct Staging {
+    double* q[2] = {nullptr, nullptr};
+    double* r[2] = {nullptr, nullptr};
+    double* norm_dev = nullptr;
+    double* norm_host = nullptr;   // page-locked
+    int norm_cap = 0;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t in[2] = {}, done[2] = {}, out[2] = {}, start = nullptr, fin = nullptr;
+    bool ready = false;
+    ~Staging() {
+      for (int s = 0; s < 2; ++s) {
+        cudaFree(q[s]);
+        cudaFree(r[s]);
+        if (ready) {
+          cudaEventDestroy(in[s]);
+          cudaEventDestroy(done[s]);
+          cudaEventDestroy(out[s]);
+        }
+      }
+      cudaFree(norm_dev);
+      cudaFreeHost(norm_host);
+      if (ready) {
+        cudaEventDestroy(start);
+        cudaEventDestroy(fin);
+        cudaStreamDestroy(h2d);
+        cudaStreamDestroy(d2h);
+      }
+    }
+  } stage;
 };
 
 struct tdg_transfer {
@@ -667,6 +698,75 @@ int tdg_residual(tdg_plan* p, const double* Q, const double* S, double* R, doubl
   a.out = R;
   a.norm = rnorm;
   return dispatch_eval<MODE_R>(p, Q, 0, a, st);
+}
+
+int tdg_residual_host(tdg_plan* p, int32_t nbatch, const double* const* Qh, const double* S,
+                      double* const* Rh, double* rnorm_host, void* stream) {
+  if (!p || (nbatch > 0 && (!Qh || !Rh))) return fail(TDG_E_ARG, "null argument");
+  if (nbatch < 0) return fail(TDG_E_ARG, "nbatch must be >= 0");
+  for (int b = 0; b < nbatch; ++b)
+    if (!Qh[b] || !Rh[b]) return fail(TDG_E_ARG, "null host buffer in batch");
+  if (nbatch == 0) return TDG_OK;
+  cudaStream_t st = as_stream(stream);
+  auto& g = p->stage;
+  const size_t bytes = static_cast<size_t>(p->nodes) * p->nv * sizeof(double);
+  if (!g.ready) {
+    for (int s = 0; s < 2; ++s) {
+      CUDA_TRY(cudaMalloc(&g.q[s], bytes ? bytes : 8));
+      CUDA_TRY(cudaMalloc(&g.r[s], bytes ? bytes : 8));
+      CUDA_TRY(cudaEventCreateWithFlags(&g.in[s], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&g.done[s], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&g.out[s], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventCreateWithFlags(&g.start, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&g.fin, cudaEventDisableTiming));
+    CUDA_TRY(cudaStreamCreateWithFlags(&g.h2d, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&g.d2h, cudaStreamNonBlocking));
+    g.ready = true;
+  }
+  if (g.norm_cap < nbatch) {
+    cudaFree(g.norm_dev);
+    cudaFreeHost(g.norm_host);
+    g.norm_dev = nullptr;
+    g.norm_host = nullptr;
+    g.norm_cap = 0;
+    CUDA_TRY(cudaMalloc(&g.norm_dev, sizeof(double) * nbatch));
+    CUDA_TRY(cudaMallocHost(&g.norm_host, sizeof(double) * nbatch));
+    g.norm_cap = nbatch;
+  }
+  // everything below is ordered after the caller's prior work on `stream`
+  CUDA_TRY(cudaEventRecord(g.start, st));
+  CUDA_TRY(cudaStreamWaitEvent(g.h2d, g.start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(g.d2h, g.start, 0));
+  CUDA_TRY(cudaMemsetAsync(g.norm_dev, 0, sizeof(double) * nbatch, st));
+  for (int b = 0; b < nbatch; ++b) {
+    const int s = b & 1;
+    // slot s is free for input once evaluation b-2 finished, for output once
+    // its device->host copy finished
+    if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(g.h2d, g.done[s], 0));
+    CUDA_TRY(cudaMemcpyAsync(g.q[s], Qh[b], bytes, cudaMemcpyHostToDevice, g.h2d));
+    CUDA_TRY(cudaEventRecord(g.in[s], g.h2d));
+    CUDA_TRY(cudaStreamWaitEvent(st, g.in[s], 0));
+    if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(st, g.out[s], 0));
+    FluxArgs a{};
+    a.S = S;
+    a.out = g.r[s];
+    a.norm = g.norm_dev + b;
+    int rc = dispatch_eval<MODE_R>(p, g.q[s], 0, a, st);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(g.done[s], st));
+    CUDA_TRY(cudaStreamWaitEvent(g.d2h, g.done[s], 0));
+    CUDA_TRY(cudaMemcpyAsync(Rh[b], g.r[s], bytes, cudaMemcpyDeviceToHost, g.d2h));
+    CUDA_TRY(cudaEventRecord(g.out[s], g.d2h));
+  }
+  CUDA_TRY(cudaMemcpyAsync(g.norm_host, g.norm_dev, sizeof(double) * nbatch, cudaMemcpyDeviceToHost,
+                           g.d2h));
+  CUDA_TRY(cudaEventRecord(g.fin, g.d2h));
+  CUDA_TRY(cudaStreamWaitEvent(st, g.fin, 0));
+  CUDA_TRY(cudaEventSynchronize(g.fin));
+  if (rnorm_host) std::memcpy(rnorm_host, g.norm_host, sizeof(double) * nbatch);
+  p->traces_of = nullptr;   // the staging slots are not caller buffers
+  return TDG_OK;
 }
 
 int tdg_tau(tdg_plan* p, const double* Q, const double* S, double* tau, int isolated,

@@ -436,6 +436,34 @@ class DGOperator:
         """r = S - M^-1 F(Q) (operators.py:344-350)."""
         return self.residual_device(Q, source, out=self.new_field())
 
+    def residual_host(self, states, source: NodalField | None = None, out=None):
+        """r = S - M^-1 F(Q) for a batch of HOST states (operators.py:344-350
+        takes and returns host arrays).
+
+        ``states``: CPU float64 tensors in the device field layout (page-locked
+        for copy/compute overlap).  Returns (list of CPU residual tensors, list
+        of max|r|).  The copies of neighbouring states overlap each evaluation
+        (tdg_residual_host)."""
+        import ctypes as C
+
+        import torch
+
+        n = self.orders.num_nodes * self.nv
+        for q in states:
+            if q.device.type != "cpu" or q.dtype != torch.float64 or q.numel() != n or not q.is_contiguous():
+                raise ValueError("host states must be contiguous CPU float64 tensors of the field size")
+        if out is None:
+            out = [torch.empty(n, dtype=torch.float64, pin_memory=True) for _ in states]
+        nb = len(states)
+        self.calls["apply"] += nb
+        src = self.source if source is None else source
+        qp = (C.c_void_p * nb)(*[q.data_ptr() for q in states])
+        rp = (C.c_void_p * nb)(*[r.data_ptr() for r in out])
+        norms = (C.c_double * nb)()
+        _lib.call("tdg_residual_host", self._plan, nb, qp, _lib.ptr(src.data if src is not None else None),
+                  rp, norms, self._stream())
+        return out, list(norms)
+
     def residual_norm(self, Q: NodalField, source: NodalField | None = None) -> float:
         import torch
 

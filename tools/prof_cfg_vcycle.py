@@ -23,3 +23,4 @@ kt = _lib.timing_read()
 print(w.name, "levels", len(s.levels), "v-cycle ms events %.2f wall %.2f kernels %.2f launches/cycle %d" % (
     e0.elapsed_time(e1) / cycles, wall * 1e3, sum(v[0] for v in kt.values()) / cycles,
     sum(v[1] for v in kt.values()) // cycles))
+print({k: (round(v[0] / cycles, 3), v[1] // cycles) for k, v in kt.items() if v[1]})
