@@ -70,7 +70,10 @@ class DGOperator:
         self.calls = {"apply": 0, "apply_isolated": 0}
         self._plan = None
         self._build()
-        self.source = (self.project_function(law.source) if getattr(law, "source", None) is not None
+        # a source-free law's S is the zero field: kernels are handed NULL for it
+        # (no 40 B/node read) whenever it is the operator's own source
+        self._zero_source = getattr(law, "source", None) is None
+        self.source = (self.project_function(law.source) if not self._zero_source
                        else NodalField.zeros(orders, self.nv, device))
 
     # --- construction ------------------------------------------------------------
@@ -423,12 +426,19 @@ class DGOperator:
                   _lib.ptr(out.data), int(bool(isolated)), self._stream())
         return out
 
+    def _src_ptr(self, src):
+        """Device pointer of a source field; NULL (zero) for None and for the
+        zero source of a source-free law."""
+        if src is None or (src is self.source and self._zero_source):
+            return None
+        return _lib.ptr(src.data)
+
     def residual_device(self, Q, source=None, out=None, norm=None):
         """r = S - A(Q) into ``out`` (nullable), max|r| into device scalar ``norm``."""
         self._check_field(Q)
         self.calls["apply"] += 1
         src = self.source if source is None else source
-        _lib.call("tdg_residual", self._plan, _lib.ptr(Q.data), _lib.ptr(src.data if src is not None else None),
+        _lib.call("tdg_residual", self._plan, _lib.ptr(Q.data), self._src_ptr(src),
                   _lib.ptr(out.data if out is not None else None), _lib.ptr(norm), self._stream())
         return out
 
@@ -460,7 +470,7 @@ class DGOperator:
         qp = (C.c_void_p * nb)(*[q.data_ptr() for q in states])
         rp = (C.c_void_p * nb)(*[r.data_ptr() for r in out])
         norms = (C.c_double * nb)()
-        _lib.call("tdg_residual_host", self._plan, nb, qp, _lib.ptr(src.data if src is not None else None),
+        _lib.call("tdg_residual_host", self._plan, nb, qp, self._src_ptr(src),
                   rp, norms, self._stream())
         return out, list(norms)
 
@@ -482,7 +492,7 @@ class DGOperator:
         self.calls["apply_isolated" if isolated else "apply"] += 1
         out = out if out is not None else torch.zeros(self.orders.num_elements, dtype=torch.float64,
                                                       device=self.device)
-        _lib.call("tdg_tau", self._plan, _lib.ptr(Q.data), _lib.ptr(self.source.data), _lib.ptr(out),
+        _lib.call("tdg_tau", self._plan, _lib.ptr(Q.data), self._src_ptr(self.source), _lib.ptr(out),
                   int(bool(isolated)), self._stream())
         return out
 
@@ -563,6 +573,6 @@ class DGOperator:
         evaluation on this operator (the next stage or sweep of a smoothing
         run), so the library may reuse the side traces that stage left."""
         _lib.call("tdg_rk3_stage_ex", self._plan, _lib.ptr(Q.data), _lib.ptr(W.data),
-                  _lib.ptr(S.data if S is not None else None), int(stage), _lib.ptr(dt), int(bool(local)),
+                  self._src_ptr(S), int(stage), _lib.ptr(dt), int(bool(local)),
                   _lib.ptr(rnorm), _lib.ptr(nonfinite), _lib.RK_TRACES_FRESH if fresh else 0,
                   self._stream())
