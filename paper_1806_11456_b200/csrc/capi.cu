@@ -145,6 +145,8 @@ struct tdg_plan {
   const double* traces_of = nullptr;
   bool rk_traces = false;   // LGL, no nonconforming face, no TMA kernel
   size_t smem_lift = 0, smem_flux = 0;
+  int elem_threads = ELEM_THREADS;   // block size of the lift / flux kernels
+  int max_tot = MAXN;                // largest work item (nodes)
   int64_t side_nodes = 0;
   int iso = -1;          // isotropic order of a single-bucket plan, else -1
   bool tma = false;      // persistent TMA-pipelined flux kernel (TDG_TMA=1 enables)
@@ -224,20 +226,24 @@ int with_nx(int iso, F&& f) {
 
 template <int LAW>
 int setup_attrs(tdg_plan* p) {
+  // The limit is a per-function, process-wide attribute shared by every
+  // plan: set it to the MAXN-item bound, never to this plan's (smaller) need.
+  const size_t ngv = p->ngv, ng = 3 * ngv, nv = p->nv, b = MAXN * sizeof(double);
+  const size_t lift = std::max(ngv + 9, ng) * b, own = (ngv + 9) * b, flux = 3 * nv * b;
   int rc = with_nx<LAW>(p->iso, [&](auto nx) -> int {
     constexpr int NX = decltype(nx)::value;
     int r;
-    if ((r = allow_smem(k_vol_lift<LAW, NX>, p->smem_lift))) return r;
-    if ((r = allow_smem(k_vol_lift_own<LAW, NX>, p->smem_lift_own))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX>, p->smem_flux))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX>, p->smem_flux))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX>, p->smem_flux))) return r;
+    if ((r = allow_smem(k_vol_lift<LAW, NX>, lift))) return r;
+    if ((r = allow_smem(k_vol_lift_own<LAW, NX>, own))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX>, flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX>, flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX>, flux))) return r;
     return TDG_OK;
   });
   if (rc) return rc;
   // cold modes and the opt-in TMA kernel use runtime orders only
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, -1>, p->smem_flux))) return rc;
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, -1>, p->smem_flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, -1>, flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, -1>, flux))) return rc;
   const size_t tb = p->smem_flux_tma;
   if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_F, -1>, tb))) return rc;
   if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_A, -1>, tb))) return rc;
@@ -277,9 +283,9 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st, boo
       if (d.ncface > 0) {
         KTimer kt(flux ? TDG_K_FACE_FLUX : TDG_K_FACE_LIFT, st);
         if (flux)
-          k_face<LAW, true><<<d.ncface, FACE_THREADS, 0, st>>>(d);
+          k_face<LAW, true><<<(d.ncface + d.face_pack - 1) / d.face_pack, d.face_threads, 0, st>>>(d);
         else
-          k_face<LAW, false><<<d.ncface, FACE_THREADS, 0, st>>>(d);
+          k_face<LAW, false><<<(d.ncface + d.face_pack - 1) / d.face_pack, d.face_threads, 0, st>>>(d);
         LAUNCH_CHECK("k_face");
       }
       if (d.nmface > 0) {
@@ -304,9 +310,9 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st, boo
       const bool own = d.family == TDG_LGL && (isolated || d.nmface == 0);
       with_nx<LAW>(p->iso, [&](auto nx) -> int {
         if (own)
-          k_vol_lift_own<LAW, decltype(nx)::value><<<d.nwork, ELEM_THREADS, p->smem_lift_own, st>>>(d, Q);
+          k_vol_lift_own<LAW, decltype(nx)::value><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q);
         else
-          k_vol_lift<LAW, decltype(nx)::value><<<d.nwork, ELEM_THREADS, p->smem_lift, st>>>(d, Q, coupled);
+          k_vol_lift<LAW, decltype(nx)::value><<<d.nwork, p->elem_threads, p->smem_lift, st>>>(d, Q, coupled);
         return 0;
       });
     }
@@ -329,11 +335,11 @@ int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cuda
       k_vol_flux_tma<LAW, MODE, -1><<<grid, TMA_THREADS, p->smem_flux_tma, st>>>(p->d, Q, a);
     } else if (hot) {
       with_nx<LAW>(p->iso, [&](auto nx) -> int {
-        k_vol_flux<LAW, MODE, hot ? decltype(nx)::value : -1><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a);
+        k_vol_flux<LAW, MODE, hot ? decltype(nx)::value : -1><<<p->d.nwork, p->elem_threads, p->smem_flux, st>>>(p->d, Q, a);
         return 0;
       });
     } else {
-      k_vol_flux<LAW, MODE, -1><<<p->d.nwork, ELEM_THREADS, p->smem_flux, st>>>(p->d, Q, a);
+      k_vol_flux<LAW, MODE, -1><<<p->d.nwork, p->elem_threads, p->smem_flux, st>>>(p->d, Q, a);
     }
   }
   LAUNCH_CHECK("k_vol_flux");
@@ -508,6 +514,21 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     if (!rc && !mfv.empty()) rc = p->mem.upload(mfv.data(), mfv.size(), &mf_d);
     d.ncface = static_cast<int>(cfv.size());
     d.nmface = static_cast<int>(mfv.size());
+    {
+      // uniform small conforming faces: several per k_face block
+      int nmu = -1;
+      for (int f : cfv) {
+        const int* fi = desc->face_info + 12 * f;
+        const int nm = (fi[9] + 1) * (fi[10] + 1);
+        if (nmu < 0) nmu = nm;
+        if (nm != nmu) { nmu = 0; break; }
+      }
+      d.face_nm = nmu > 0 ? nmu : 0;
+      // measured: 128-thread blocks pay off when they hold >= 3 faces (N <= 5);
+      // 49- and 64-node faces run best one per 64-thread block
+      d.face_pack = nmu > 0 ? (3 * nmu <= FACE_THREADS_MAX ? FACE_THREADS_MAX : FACE_THREADS) / nmu : 1;
+      d.face_threads = nmu > 0 ? (d.face_pack * nmu + 31) / 32 * 32 : FACE_THREADS;
+    }
     d.cface = cf_d;
     d.mface = mf_d;
     int4* fd_d = nullptr;
@@ -570,6 +591,16 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     work.push_back(make_int2(s, e - s));
     s = e;
   }
+  // element-kernel block size: enough threads for the largest item at NPT
+  // nodes per thread (a 343-node N=6 item runs 192 threads, not 256)
+  long long max_tot = 1;
+  for (const int2& w : work) {
+    const int* o = &p->orders_h[3 * w.x];
+    max_tot = std::max<long long>(max_tot, static_cast<long long>(w.y) * (o[0] + 1) * (o[1] + 1) * (o[2] + 1));
+  }
+  p->elem_threads = static_cast<int>(std::min<long long>(
+      ELEM_THREADS, std::max<long long>(128, (max_tot + NPT * 32 - 1) / (NPT * 32) * 32)));
+  p->max_tot = static_cast<int>(max_tot);
   std::vector<int4> iso, bnd;
   iso.reserve(6 * ns);
   for (int s = 0; s < ns; ++s)
@@ -627,13 +658,15 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.gtr = gtr;
   d.fsurf = fsurf;
   d.grad = grad;
-  p->smem_lift = static_cast<size_t>(std::max(p->ngv + 9, NG)) * MAXN * sizeof(double);
+  // dynamic shared memory sized by the largest work item (<= MAXN nodes)
+  const size_t mt = static_cast<size_t>(p->max_tot);
+  p->smem_lift = static_cast<size_t>(std::max(p->ngv + 9, NG)) * mt * sizeof(double);
   {
     bool curved = false;
     for (int s = 0; s < ns && !curved; ++s) curved = desc->affine[s] == 0;
-    p->smem_lift_own = static_cast<size_t>(p->ngv + (curved ? 9 : 0)) * MAXN * sizeof(double);
+    p->smem_lift_own = static_cast<size_t>(p->ngv + (curved ? 9 : 0)) * mt * sizeof(double);
   }
-  p->smem_flux = static_cast<size_t>(3 * p->nv) * MAXN * sizeof(double);
+  p->smem_flux = static_cast<size_t>(3 * p->nv) * mt * sizeof(double);
   p->smem_flux_tma = static_cast<size_t>(p->nv == 5 ? tma_flux_smem_doubles<5, 12>()
                                                     : tma_flux_smem_doubles<1, 3>()) * sizeof(double);
   {

@@ -17,6 +17,7 @@ constexpr int ELEM_THREADS = 256;     // element kernels: 8 warps
 constexpr int MAXN = 512;             // nodes per element work item (<= (7+1)^3)
 constexpr int NPT = MAXN / ELEM_THREADS;
 constexpr int FACE_THREADS = 64;      // one interior face (<= 8x8 mortar nodes) per block
+constexpr int FACE_THREADS_MAX = 128; // packed uniform faces: face_pack * face_nm <= 128
 constexpr int SIDE_THREADS = 256;     // four element sides per block
 constexpr int SIDES_PER_BLOCK = SIDE_THREADS / 64;
 
@@ -66,6 +67,9 @@ struct DevPlan {
   // L1 | L2<<3 | R1<<6 | R2<<9 aligned own orders)
   const int4* fdesc;
   int ncface, nmface;
+  // k_face packing: when every conforming face has the same node count
+  // face_nm, a block of face_threads evaluates face_pack = 128 / face_nm faces
+  int face_pack, face_nm, face_threads;
   const int* cface;              // conforming interior faces (k_face)
   const int* mface;              // nonconforming interior faces (k_mortar)
   // scratch (device)

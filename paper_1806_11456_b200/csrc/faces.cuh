@@ -78,14 +78,17 @@ __device__ __forceinline__ void face_point(const DevPlan& P, const double* qsrc,
 // own-order traces align node for node (up to orientation), and the signed
 // values go straight into the per-side own-order surface arrays.
 template <int LAW, bool FLUX>
-__global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
+__global__ void __launch_bounds__(FACE_THREADS_MAX) k_face(DevPlan P) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   constexpr int COUT = FLUX ? NV : NG;
-  const int t = threadIdx.x;
-  if (t == 0) {
+  // face_pack > 1: this block's threads are face_pack groups of face_nm
+  const int fl = P.face_pack > 1 ? threadIdx.x / P.face_nm : 0;
+  const int t = threadIdx.x - fl * P.face_nm;
+  const int fi = blockIdx.x * P.face_pack + fl;
+  if (threadIdx.x == 0) {
     // L2 prefetch of the face about one wave ahead
-    const int ba = blockIdx.x + P.pf_face * P.nsm;
+    const int ba = fi + P.pf_face * P.nsm * P.face_pack;
     if (ba < P.ncface) {
       const int4 fn = P.fdesc[2 * (P.nmface ? P.cface[ba] : ba)];
       const int mn = ((fn.z & 7) + 1) * (((fn.z >> 3) & 7) + 1);
@@ -98,7 +101,8 @@ __global__ void __launch_bounds__(FACE_THREADS) k_face(DevPlan P) {
       }
     }
   }
-  const int f = P.nmface ? P.cface[blockIdx.x] : blockIdx.x;   // all conforming: identity list
+  if (fi >= P.ncface || fl >= P.face_pack) return;
+  const int f = P.nmface ? P.cface[fi] : fi;   // all conforming: identity list
   const int4 fd = P.fdesc[2 * f];
   const int M1 = fd.z & 7, M2 = (fd.z >> 3) & 7, orient = (fd.z >> 6) & 7;
   const int nm = (M1 + 1) * (M2 + 1);

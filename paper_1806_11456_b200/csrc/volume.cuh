@@ -72,7 +72,7 @@ __device__ __forceinline__ void item_side_traces(const DevPlan& P, int slot0, in
                                                  Vol vol) {
   const bool lgl = P.family == 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int task = warp; task < E * 6; task += ELEM_THREADS / 32) {
+  for (int task = warp; task < E * 6; task += blockDim.x >> 5) {
     const int e = task / 6, s = task % 6, slot = slot0 + e;
     int d, a, b;
     side_dirs(s, d, a, b);
@@ -154,6 +154,42 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
   const int np[3] = {No[0] + 1, No[1] + 1, No[2] + 1};
   const int n = np[0] * np[1] * np[2];
   const int strides[3] = {1, np[0], np[0] * np[1]};
+  if (!coupled || P.nmface == 0) {
+    // every side on own-order traces: (element, side, face node) flattened
+    // over the block, so small faces do not leave warps mostly idle
+    const int nfs[3] = {np[1] * np[2], np[0] * np[2], np[0] * np[1]};
+    const int per_e = 2 * (nfs[0] + nfs[1] + nfs[2]);
+    const bool lgl = P.family == 1;
+    for (int u = threadIdx.x; u < wi.y * per_e; u += blockDim.x) {
+      const int e = u / per_e;
+      int r = u - e * per_e, s = 0;
+      while (r >= nfs[s >> 1]) {
+        r -= nfs[s >> 1];
+        ++s;
+      }
+      int d, a, b;
+      side_dirs(s, d, a, b);
+      const int na = np[a], nf = nfs[d], nd = np[d];
+      const int ib = r / na, ia = r - ib * na;
+      const int slot = wi.x + e;
+      const double* q = Q + P.node_off[slot] * NV + ia * strides[a] + ib * strides[b];
+      double* dst = P.qtr + P.side_off[slot * 6 + s] * NV + r;
+      const int sd = strides[d];
+      const double* row = &sb[d][(s & 1) * 8];
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        double acc;
+        if (lgl) {
+          acc = q[(long long)c * n + ((s & 1) ? (nd - 1) * sd : 0)];
+        } else {
+          acc = 0.0;
+          for (int m = 0; m < nd; ++m) acc += row[m] * q[(long long)c * n + m * sd];
+        }
+        dst[(long long)c * nf] = acc;
+      }
+    }
+    return;
+  }
   item_side_traces<NV>(P, wi.x, wi.y, coupled, np, strides, sb, P.qtr, P.qtrm,
                            [&](int e, int c, int off) {
                              return Q[(P.node_off[wi.x + e] * NV) + (long long)c * n + off];
@@ -321,7 +357,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
 
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * ELEM_THREADS;
+    const int t = threadIdx.x + r * blockDim.x;
     if (t < tot) {
       const int e = t / n, node = t - e * n, slot = wi.x + e;
       const long long base = P.node_off[slot] * NV;
@@ -344,7 +380,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
   double Greg[NPT][NG];
 #pragma unroll
   for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * ELEM_THREADS;
+    const int t = threadIdx.x + r * blockDim.x;
     if (t < tot) {
       const int e = t / n, node = t - e * n, slot = wi.x + e;
       const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
@@ -356,7 +392,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
   double* G = sm;   // [NG][tot]
 #pragma unroll
   for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * ELEM_THREADS;
+    const int t = threadIdx.x + r * blockDim.x;
     if (t < tot) {
       const int e = t / n, node = t - e * n, slot = wi.x + e;
       const long long gb = P.node_off[slot] * NG;
@@ -409,7 +445,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
   const bool aff = s_aff != 0;
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * ELEM_THREADS;
+    const int t = threadIdx.x + r * blockDim.x;
     if (t < tot) {
       const int e = t / n, node = t - e * n, slot = wi.x + e;
       const long long base = P.node_off[slot] * NV;
@@ -431,7 +467,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
   const int np[3] = {n1p, n2p, n3p};
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * ELEM_THREADS;
+    const int t = threadIdx.x + r * blockDim.x;
     if (t < tot) {
       const int e = t / n, node = t - e * n, slot = wi.x + e;
       const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
@@ -495,7 +531,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
 
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * ELEM_THREADS;
+    const int t = threadIdx.x + r * blockDim.x;
     if (t < tot) {
       const int e = t / n, node = t - e * n, slot = wi.x + e;
       const long long base = P.node_off[slot] * NV;
@@ -528,7 +564,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   double rmax = 0.0;
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * ELEM_THREADS;
+    const int t = threadIdx.x + r * blockDim.x;
     if (t < tot) {
       const int e = t / n, node = t - e * n, slot = wi.x + e;
       const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);

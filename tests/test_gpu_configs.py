@@ -68,6 +68,37 @@ def test_config1_protocol_matches_oracle():
                 assert abs(tm.tau[e][d][n] - v) <= 1e-12 * scale
 
 
+def test_config4_reduced_protocol_matches_oracle():
+    """Config 4's protocol (N=7 Taylor-Green state, 7-level V-cycles 7..1 with
+    2/2/2 pinned sweeps) on a 3^3 box: residual histories vs the oracle to
+    1e-10, identical phase/sweep logs, final states to 1e-10."""
+    from oracle import multigrid as omg
+    from oracle.fields import OrderField as OO
+    from paper_1806_11456_b200 import configs, multigrid
+
+    w = configs.config4(n=3)
+    law = oracle_law(w.law)
+    s = multigrid.FASSolver(w.mesh, w.law, w.orders, smoother=multigrid.SmootherConfig(**w.smoother),
+                            family=w.family, form=w.form)
+    s.set_state(s.finest.op.project_function(w.init))
+    so = omg.FASSolver(w.mesh, law, OO(np.asarray(w.orders.orders)), smoother=omg.SmootherConfig(**w.smoother),
+                       family=w.family, form=w.form)
+    so.set_state(so.finest.op.project_function(w.init))
+    assert len(s.levels) == len(so.levels) == 7
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for _ in range(2):
+            s.v_cycle()
+            so.v_cycle()
+    rn = np.array([r["rnorm"] for r in s.log])
+    rno = np.array([r["rnorm"] for r in so.log])
+    assert [(r["level"], r["phase"], r["sweeps"]) for r in s.log] == \
+           [(r["level"], r["phase"], r["sweeps"]) for r in so.log]
+    assert np.abs(rn - rno).max() <= 1e-10 * rno.max()
+    Qf = _to_oracle(s.finest.Q, so.Q.field)
+    assert (Qf - so.Q).norm_inf() <= 1e-10 * so.Q.norm_inf()
+
+
 def test_config3_sample_matches_oracle():
     from oracle import timestep as ots
     from oracle.fields import OrderField as OO
