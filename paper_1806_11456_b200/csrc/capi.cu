@@ -610,9 +610,17 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     const long long go = desc->ghost_off[f];
     bnd.push_back(make_int4(b[0], b[1], b[2], static_cast<int>(go)));
   }
+  std::vector<int> work_aff(work.size());
+  for (size_t k = 0; k < work.size(); ++k) {
+    int a = 1;
+    for (int e = 0; e < work[k].y; ++e) a &= desc->affine[work[k].x + e] != 0;
+    work_aff[k] = a;
+  }
   int2* work_d;
+  int* work_aff_d = nullptr;
   int4 *iso_d, *bnd_d;
   rc = p->mem.upload(work.data(), work.size(), &work_d);
+  if (!rc) rc = p->mem.upload(work_aff.data(), work_aff.size(), &work_aff_d);
   if (!rc) rc = p->mem.upload(iso.data(), iso.size(), &iso_d);
   if (!rc) rc = p->mem.upload(bnd.data(), bnd.size(), &bnd_d);
   const size_t sn = static_cast<size_t>(desc->side_nodes);
@@ -647,6 +655,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     d.pf_down = knob("TDG_PF_DOWN", 5);
   }
   d.work = work_d;
+  d.work_aff = work_aff_d;
   d.nside_iso = static_cast<int>(iso.size());
   d.side_iso = iso_d;
   d.nside_bnd = static_cast<int>(bnd.size());

@@ -49,6 +49,7 @@ struct DevPlan {
   // element work items: (first slot, count), uniform orders inside an item
   int nwork;
   const int2* work;
+  const int* work_aff;   // per work item: 1 if every element of the item is affine
   int nsm;        // SMs: kernels prefetch the work about one wave ahead (L2)
   int pf_trace, pf_face, pf_down;   // look-ahead distances, blocks per SM
   // side work items for side kernels: (slot, side | kind<<8), ghost offset

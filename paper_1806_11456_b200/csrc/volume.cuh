@@ -322,6 +322,50 @@ __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T,
   for (int c = 0; c < NG; ++c) out[c] = acc[c] * invm;
 }
 
+// This thread's NPT nodes' state, loaded before the block's table barrier so
+// that the loads are in flight while the spectral tables are staged.
+template <int NV>
+__device__ __forceinline__ void load_item_state(const DevPlan& P, const double* __restrict__ Q, int2 wi,
+                                                int n, int tot, double (&q)[NPT][NV]) {
+#pragma unroll
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * blockDim.x;
+    if (t < tot) {
+      const int e = t / n, node = t - e * n;
+      const long long base = P.node_off[wi.x + e] * NV;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) q[r][v] = Q[base + (long long)v * n + node];
+    }
+  }
+}
+
+// Stage g(q) (and, on curved items, the 9 metric terms Ja) for the thread's
+// nodes in shared memory.
+template <int LAW>
+__device__ __forceinline__ void stage_grad_vars(const DevPlan& P, int2 wi, int n, int tot, bool aff,
+                                                const double (&q)[NPT][Law<LAW>::NV], double* gs,
+                                                double* js) {
+  using L = Law<LAW>;
+  constexpr int NGV = L::NGV;
+#pragma unroll
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * blockDim.x;
+    if (t < tot) {
+      double g[NGV];
+      L::grad_vars(P.prm, q[r], g);
+#pragma unroll
+      for (int k = 0; k < NGV; ++k) gs[k * tot + t] = g[k];
+      if (!aff) {
+        const int e = t / n, node = t - e * n;
+        int ms;
+        const double* m = metric_ptr(P, wi.x + e, node, n, ms);
+#pragma unroll
+        for (int c = 0; c < 9; ++c) js[c * tot + t] = m[(1 + c) * ms];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // BR1 lift, volume part + scatter of the face contributions, times M^-1
 // (operators.py:224-265); writes the gradient and its side traces.
@@ -336,45 +380,22 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
-  __shared__ int s_aff;
   extern __shared__ double sm[];
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.orders + 3 * wi.x;
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
-  prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
-  load_tables(P, N1, N2, N3, T);
-  if (threadIdx.x == 0) {
-    int a = 1;
-    for (int e = 0; e < wi.y; ++e) a &= P.affine[wi.x + e] != 0;
-    s_aff = a;
-  }
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
+  double qa[NPT][NV];
+  load_item_state<NV>(P, Q, wi, n, tot, qa);
+  prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+  load_tables(P, N1, N2, N3, T);
+  const bool aff = P.work_aff[blockIdx.x] != 0;
   double* gs = sm;               // [NGV][tot]
   double* js = sm + NGV * tot;   // [9][tot]  (curved items only)
-  __syncthreads();
-  const bool aff = s_aff != 0;
+  // staging needs no table: one barrier covers both
+  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
 
-#pragma unroll 1
-  for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * blockDim.x;
-    if (t < tot) {
-      const int e = t / n, node = t - e * n, slot = wi.x + e;
-      const long long base = P.node_off[slot] * NV;
-      double q[NV], g[NGV];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) q[v] = Q[base + (long long)v * n + node];
-      L::grad_vars(P.prm, q, g);
-#pragma unroll
-      for (int k = 0; k < NGV; ++k) gs[k * tot + t] = g[k];
-      if (!aff) {
-        int ms;
-        const double* m = metric_ptr(P, slot, node, n, ms);
-#pragma unroll
-        for (int c = 0; c < 9; ++c) js[c * tot + t] = m[(1 + c) * ms];
-      }
-    }
-  }
   __syncthreads();
 
   double Greg[NPT][NG];
@@ -425,44 +446,21 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
-  __shared__ int s_aff;
   extern __shared__ double sm[];
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.orders + 3 * wi.x;
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
-  prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
-  load_tables(P, N1, N2, N3, T);
-  if (threadIdx.x == 0) {
-    int a = 1;
-    for (int e = 0; e < wi.y; ++e) a &= P.affine[wi.x + e] != 0;
-    s_aff = a;
-  }
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
+  double qa[NPT][NV];
+  load_item_state<NV>(P, Q, wi, n, tot, qa);
+  prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+  load_tables(P, N1, N2, N3, T);
+  const bool aff = P.work_aff[blockIdx.x] != 0;
   double* gs = sm;               // [NGV][tot]
   double* js = sm + NGV * tot;   // [9][tot]  (curved items only)
-  __syncthreads();
-  const bool aff = s_aff != 0;
-#pragma unroll 1
-  for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * blockDim.x;
-    if (t < tot) {
-      const int e = t / n, node = t - e * n, slot = wi.x + e;
-      const long long base = P.node_off[slot] * NV;
-      double q[NV], g[NGV];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) q[v] = Q[base + (long long)v * n + node];
-      L::grad_vars(P.prm, q, g);
-#pragma unroll
-      for (int k = 0; k < NGV; ++k) gs[k * tot + t] = g[k];
-      if (!aff) {
-        int ms;
-        const double* m = metric_ptr(P, slot, node, n, ms);
-#pragma unroll
-        for (int c = 0; c < 9; ++c) js[c * tot + t] = m[(1 + c) * ms];
-      }
-    }
-  }
+  // staging needs no table: one barrier covers both
+  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
   __syncthreads();
   const int np[3] = {n1p, n2p, n3p};
 #pragma unroll 1
@@ -527,7 +525,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   const int n = n1p * n2p * n3p, tot = wi.y * n;
   const bool visc = L::viscous(P.prm);
   double* ft = sm;   // [3][NV][tot]
-  __syncthreads();
+  // the contravariant fluxes need no table: the barrier after them covers both
 
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
