@@ -520,12 +520,12 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   // epilogue inputs, read after the contraction
   if (MODE != MODE_F) prefetch_item_nodes<NV>(P, MODE == MODE_A ? A.X : A.S, wi, 32);
   if (MODE == MODE_RK && A.stage != 0) prefetch_item_nodes<NV>(P, A.W, wi, 64);
-  load_tables(P, N1, N2, N3, T);
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
   const bool visc = L::viscous(P.prm);
   double* ft = sm;   // [3][NV][tot]
-  // the contravariant fluxes need no table: the barrier after them covers both
+  // the contravariant fluxes need no table: they are formed first, the
+  // tables are staged after them, and one barrier covers both
 
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
@@ -557,6 +557,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
       }
     }
   }
+  load_tables(P, N1, N2, N3, T);
   __syncthreads();
 
   double rmax = 0.0;
