@@ -653,6 +653,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     d.pf_trace = knob("TDG_PF_TRACE", 2);
     d.pf_face = knob("TDG_PF_FACE", 4);
     d.pf_down = knob("TDG_PF_DOWN", 5);
+    d.div_mma = knob("TDG_DIV_MMA", 0);   // measured slower (extra barriers, serial directions); opt-in
   }
   d.work = work_d;
   d.work_aff = work_aff_d;

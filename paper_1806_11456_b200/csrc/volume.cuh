@@ -507,6 +507,72 @@ struct FluxArgs {
   int traces;          // RK: also write the new state's own-order Q traces (LGL, conforming)
 };
 
+// ---------------------------------------------------------------------------
+// Weak divergence on the FP64 tensor cores (operators.py:196-200): for each
+// direction d and component c, the item's d-lines (all E elements, same
+// orders) are contracted 8 lines at a time with the weighted derivative
+// matrix, D(i, line) = sum_m Dhat_d[m][i] ft_d[c](m, line) (mma.m8n8k4, one
+// or two k-steps), scaled by the line's tangential weights.  The result
+// accumulates in place in direction 0's array ft[0][c] (direction 0 first,
+// then += 1, then += 2: the ((x + y) + z) order of the scalar chains); each
+// tile's outputs are the nodes of its own lines, so the in-place direction-0
+// pass is warp-local.  One block barrier after each direction.  Replaces
+// ~3(N+1) shared-memory loads per node and component by 2 per 8 outputs.
+template <int C>
+__device__ __forceinline__ void item_weak_div_mma(const ElemTables& T, double* ft, int tot, int n,
+                                                  int n1p, int n2p, int n3p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int np[3] = {n1p, n2p, n3p};
+  const int st[3] = {1, n1p, n1p * n2p};
+  const int E = tot / n;
+#pragma unroll 1
+  for (int d = 0; d < 3; ++d) {
+    const int a = (d == 0) ? 1 : 0, b = (d == 2) ? 1 : 2;
+    const int nd = np[d], na = np[a], sd = st[d], sa = st[a], sb = st[b];
+    const int lines_e = na * np[b], nlines = E * lines_e, ntiles = (nlines + 7) >> 3;
+    const double a0 = (g < nd && q < nd) ? T.dh[d][q * 8 + g] : 0.0;
+    const double a1 = (g < nd && q + 4 < nd) ? T.dh[d][(q + 4) * 8 + g] : 0.0;
+    const bool k2 = nd > 4;
+    // node base and tangential weight of line L (-1: past the end)
+    auto line = [&](int L, double& w) -> int {
+      if (L >= nlines) return -1;
+      const int e = L / lines_e, r = L - e * lines_e, ib = r / na, ia = r - ib * na;
+      w = T.w[a][ia] * T.w[b][ib];
+      return e * n + ia * sa + ib * sb;
+    };
+#pragma unroll 1
+    for (int tile = warp; tile < ntiles; tile += nw) {
+      // line geometry once per tile; the C components' MMA chains interleave
+      double wl, w0, w1;
+      const int bl = line(tile * 8 + g, wl);
+      const int o0 = line(tile * 8 + 2 * q, w0), o1 = line(tile * 8 + 2 * q + 1, w1);
+      const bool l0 = bl >= 0 && q < nd, l1 = bl >= 0 && k2 && q + 4 < nd;
+      const int i0 = bl + q * sd, i1 = bl + (q + 4) * sd;
+      const bool s0 = g < nd && o0 >= 0, s1 = g < nd && o1 >= 0;
+      const int j0 = o0 + g * sd, j1 = o1 + g * sd;
+      double d0[C], d1[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const double* src = ft + (d * C + c) * tot;
+        const double b0 = l0 ? src[i0] : 0.0;
+        const double b1 = l1 ? src[i1] : 0.0;
+        d0[c] = 0.0;
+        d1[c] = 0.0;
+        dmma_8x8x4(d0[c], d1[c], a0, b0);
+        if (k2) dmma_8x8x4(d0[c], d1[c], a1, b1);
+      }
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        double* acc = ft + c * tot;
+        if (s0) acc[j0] = d == 0 ? d0[c] * w0 : acc[j0] + d0[c] * w0;
+        if (s1) acc[j1] = d == 0 ? d1[c] * w1 : acc[j1] + d1[c] * w1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <int LAW, int MODE, int NX>
 __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
   using L = Law<LAW>;
@@ -560,6 +626,8 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   load_tables(P, N1, N2, N3, T);
   __syncthreads();
 
+  const bool mma_div = P.div_mma != 0;
+  if (mma_div) item_weak_div_mma<NV>(T, ft, tot, n, n1p, n2p, n3p);
   double rmax = 0.0;
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
@@ -574,6 +642,10 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
         F[v] = 0.0;
         F0[v] = F1[v] = F2[v] = 0.0;
       }
+      if (mma_div) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) F0[v] = ft[v * tot + t];
+      } else {
       {
         const double wo = T.w[1][j] * T.w[2][k];
 #pragma unroll
@@ -606,6 +678,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
 #pragma unroll
           for (int v = 0; v < NV; ++v) F2[v] += dw * ft[(2 * NV + v) * tot + idx];
         }
+      }
       }
 #pragma unroll
       for (int v = 0; v < NV; ++v) F[v] -= (F0[v] + F1[v]) + F2[v];
