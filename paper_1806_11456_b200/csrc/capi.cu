@@ -192,6 +192,7 @@ struct tdg_transfer {
   size_t smem = 0;
   int nv = 1;
   int iso_f = 0, iso_c = 0;   // points per direction when every element is isotropic and uniform
+  bool lines = false;         // uniform pair, items contiguous on both levels: k_transfer_lines
 };
 
 namespace {
@@ -367,8 +368,29 @@ template <int MODE, int NS, int ND>
 bool launch_transfer_iso(const tdg_transfer* t, int ns, int nd, const double* in, const double* in2,
                          double* out, cudaStream_t st) {
   if (ns != NS || nd != ND) return false;
-  k_transfer<MODE, 5, NS, ND><<<t->nwork, ELEM_THREADS, t->smem, st>>>(t->d, in, in2, out);
+  if (t->lines)
+    k_transfer_lines<MODE, 5, NS, ND><<<t->nwork, ELEM_THREADS, t->smem, st>>>(t->d, in, in2, out);
+  else
+    k_transfer<MODE, 5, NS, ND><<<t->nwork, ELEM_THREADS, t->smem, st>>>(t->d, in, in2, out);
   return true;
+}
+
+template <int NS, int ND>
+int allow_lines_pair(size_t b) {
+  int rc;
+  if ((rc = allow_smem(k_transfer_lines<TR_RESTRICT, 5, NS, ND>, b))) return rc;
+  if ((rc = allow_smem(k_transfer_lines<TR_PROLONG, 5, NS, ND>, b))) return rc;
+  return allow_smem(k_transfer_lines<TR_PROLONG_ADD, 5, NS, ND>, b);
+}
+
+int allow_lines_smem(size_t b) {
+  int rc;
+  if ((rc = allow_lines_pair<8, 7>(b)) || (rc = allow_lines_pair<7, 8>(b)) || (rc = allow_lines_pair<7, 6>(b)) ||
+      (rc = allow_lines_pair<6, 7>(b)) || (rc = allow_lines_pair<6, 5>(b)) || (rc = allow_lines_pair<5, 6>(b)) ||
+      (rc = allow_lines_pair<5, 4>(b)) || (rc = allow_lines_pair<4, 5>(b)) || (rc = allow_lines_pair<4, 3>(b)) ||
+      (rc = allow_lines_pair<3, 4>(b)) || (rc = allow_lines_pair<3, 2>(b)) || (rc = allow_lines_pair<2, 3>(b)))
+    return rc;
+  return TDG_OK;
 }
 
 template <int MODE>
@@ -1010,9 +1032,26 @@ int tdg_transfer_create(const tdg_transfer_desc* desc, tdg_transfer** out) {
     };
     t->iso_f = iso_points(f_orders, ns);
     t->iso_c = iso_points(c_orders, static_cast<int>(c_orders.size() / 3));
+    // line kernel: every item is a run of consecutive slots on both levels
+    // (node offsets then advance by one element's points per slot)
+    // (TDG_TRANSFER_LINES=0 keeps the one-output-per-thread kernel)
+    const char* lenv = getenv("TDG_TRANSFER_LINES");
+    bool contig = t->iso_f > 0 && t->iso_c > 0 && !(lenv && lenv[0] == '0');
+    const long long pf = static_cast<long long>(t->iso_f) * t->iso_f * t->iso_f;
+    const long long pc = static_cast<long long>(t->iso_c) * t->iso_c * t->iso_c;
+    for (const int2& w : work) {
+      for (int e = 1; e < w.y && contig; ++e) {
+        const int s = w.x + e;
+        contig = c_of_f[s] == c_of_f[w.x] + e &&
+                 desc->fine_node_off[s] == desc->fine_node_off[w.x] + e * pf &&
+                 desc->coarse_node_off[c_of_f[s]] == desc->coarse_node_off[c_of_f[w.x]] + e * pc;
+      }
+      if (!contig) break;
+    }
+    t->lines = contig;
   }
   if ((rc = allow_smem(k_transfer<TR_RESTRICT>, t->smem)) || (rc = allow_smem(k_transfer<TR_PROLONG>, t->smem)) ||
-      (rc = allow_smem(k_transfer<TR_PROLONG_ADD>, t->smem))) {
+      (rc = allow_smem(k_transfer<TR_PROLONG_ADD>, t->smem)) || (rc = allow_lines_smem(t->smem))) {
     delete t;
     return rc;
   }

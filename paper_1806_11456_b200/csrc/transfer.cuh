@@ -114,4 +114,113 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_transfer(DevTransfer T, const 
   }
 }
 
+#ifndef TDG_TRANSFER_BLOCKS
+#define TDG_TRANSFER_BLOCKS 5   // <= 51 registers (measured best with 2 outputs per line at a time)
+#endif
+#ifndef TDG_TRANSFER_UNROLL
+#define TDG_TRANSFER_UNROLL 2   // outputs per line computed together (ILP vs registers)
+#endif
+constexpr int kTransferUnroll = TDG_TRANSFER_UNROLL;
+
+// Uniform isotropic level pairs (every fine element NS^3 -> NS^3 points, every
+// coarse element ND^3 <-> ...) whose work items are runs of consecutive slots
+// on both levels (checked at transfer creation): the item's source span is
+// one contiguous range, loaded with independent unrolled loads (PROLONG_ADD:
+// Q_c - Q_c0 formed on the fly); each pass is one 1D line per thread, held in
+// registers (NS loads -> ND outputs), instead of one output per thread
+// re-reading the line.  Same per-output summation order as k_transfer.
+template <int MODE, int NVC, int NS, int ND>
+__global__ void __launch_bounds__(ELEM_THREADS, TDG_TRANSFER_BLOCKS) k_transfer_lines(DevTransfer T, const double* __restrict__ in,
+                                                                 const double* __restrict__ in2,
+                                                                 double* __restrict__ out) {
+  extern __shared__ double sm[];
+  __shared__ double mat[64];
+  constexpr bool down = MODE == TR_RESTRICT;
+  constexpr int ns = NS * NS * NS, nd = ND * ND * ND;
+  constexpr int S1 = ND * NS * NS, S2 = ND * ND * NS;
+  constexpr int MA = ns > S2 ? ns : S2, MB = S1;
+  constexpr int R = (MAXN * NVC + ELEM_THREADS - 1) / ELEM_THREADS;
+  const int2 wi = T.work[blockIdx.x];
+  const int fs0 = wi.x, E = wi.y;
+  const int cs0 = T.c_slot_of_f[fs0];
+  const long long fb = T.f_node_off[fs0] * NVC, cb = T.c_node_off[cs0] * NVC;
+  // stage the source: E * NVC * ns contiguous values
+  const long long ib = down ? fb : cb;
+  const int tot = E * NVC * ns;
+  double x[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int u = threadIdx.x + r * ELEM_THREADS;
+    if (u < tot) {
+      x[r] = in[ib + u];
+      if (MODE == TR_PROLONG_ADD && in2) x[r] -= in2[ib + u];
+    }
+  }
+  for (int u = threadIdx.x; u < 64; u += blockDim.x)
+    mat[u] = T.tables[OFF_T + ((NS - 1) * 8 + (ND - 1)) * 64 + u];
+  double* A = sm;                      // [E*NVC][MA]
+  double* B = sm + E * NVC * MA;       // [E*NVC][MB]
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int u = threadIdx.x + r * ELEM_THREADS;
+    if (u < tot) A[(u / ns) * MA + u % ns] = x[r];
+  }
+  __syncthreads();
+  // x pass: lines (ev, jk) -> B[ev][a + ND * jk]
+  for (int L = threadIdx.x; L < E * NVC * NS * NS; L += blockDim.x) {
+    const int ev = L / (NS * NS), jk = L % (NS * NS);
+    const double* src = A + ev * MA + jk * NS;
+    double v[NS];
+#pragma unroll
+    for (int i = 0; i < NS; ++i) v[i] = src[i];
+    double* dst = B + ev * MB + jk * ND;
+#pragma unroll kTransferUnroll
+    for (int a = 0; a < ND; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int i = 0; i < NS; ++i) acc += mat[a * 8 + i] * v[i];
+      dst[a] = acc;
+    }
+  }
+  __syncthreads();
+  // y pass: lines (ev, a, k) -> A[ev][a + ND * (b + ND * k)]
+  for (int L = threadIdx.x; L < E * NVC * ND * NS; L += blockDim.x) {
+    const int ev = L / (ND * NS), r = L % (ND * NS);
+    const int a = r % ND, k = r / ND;
+    const double* src = B + ev * MB + a + ND * NS * k;
+    double v[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) v[j] = src[ND * j];
+    double* dst = A + ev * MA + a + ND * ND * k;
+#pragma unroll kTransferUnroll
+    for (int b = 0; b < ND; ++b) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NS; ++j) acc += mat[b * 8 + j] * v[j];
+      dst[ND * b] = acc;
+    }
+  }
+  __syncthreads();
+  // z pass + store: lines (ev, ab) -> out[e][v][ab + ND^2 c]
+  const long long ob = down ? cb : fb;
+  for (int L = threadIdx.x; L < E * NVC * ND * ND; L += blockDim.x) {
+    const int ev = L / (ND * ND), ab = L % (ND * ND);
+    const double* src = A + ev * MA + ab;
+    double v[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) v[k] = src[ND * ND * k];
+    double* dst = out + ob + (long long)ev * nd + ab;
+#pragma unroll kTransferUnroll
+    for (int c = 0; c < ND; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) acc += mat[c * 8 + k] * v[k];
+      if (MODE == TR_PROLONG_ADD)
+        dst[ND * ND * c] += acc;
+      else
+        dst[ND * ND * c] = acc;
+    }
+  }
+}
+
 }  // namespace tdg
