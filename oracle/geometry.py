@@ -58,6 +58,45 @@ def _d(arr, axis, D):
     return np.moveaxis(np.einsum("im,...m->...i", D, np.moveaxis(arr, axis, -1)), -1, axis)
 
 
+def affine_map(ctrl):
+    """Affine elements of the invariant-curl form: ctrl (B, a1, a2, a3, 3)
+    control nodes on the equispaced reference grid -> (mask (B,), A (B, 3, 3))
+    with A[:, d] = dX/dxi_d, the element being affine (a parallelepiped map)
+    when every control node lies within 1e-13 (relative to the edge vectors)
+    of c + sum_d A_d xi_d.  Their curl-form metrics are replaced by the exact
+    constants J = A_0 . (A_1 x A_2), Ja^i = A_j x A_k (collocated curl-form
+    round-off is ~1e-12 at N = 7, enough to move an M = 0.1 residual by
+    ~3e-11 relative); free-stream preservation is unaffected (constant
+    metrics satisfy the metric identities exactly).  Same arithmetic in the
+    product (paper_1806_11456_b200/geometry.py) and the oracle, element-wise
+    only, so both produce identical bits."""
+    x0 = ctrl[:, 0, 0, 0]
+    A = np.stack([0.5 * (ctrl[:, -1, 0, 0] - x0), 0.5 * (ctrl[:, 0, -1, 0] - x0),
+                  0.5 * (ctrl[:, 0, 0, -1] - x0)], axis=1)                 # (B, 3[d], 3[x])
+    c = x0 + A[:, 0] + A[:, 1] + A[:, 2]
+    xi = [np.linspace(-1.0, 1.0, s) for s in ctrl.shape[1:4]]
+    pred = (c[:, None, None, None, :]
+            + A[:, 0][:, None, None, None, :] * xi[0][None, :, None, None, None]
+            + A[:, 1][:, None, None, None, :] * xi[1][None, None, :, None, None]
+            + A[:, 2][:, None, None, None, :] * xi[2][None, None, None, :, None])
+    scale = np.abs(A).max(axis=(1, 2))
+    mask = (np.abs(pred - ctrl).max(axis=(1, 2, 3, 4)) <= 1e-13 * scale) & (scale > 0.0)
+    return mask, A
+
+
+def _cross3(a, b):
+    return np.stack([a[..., 1] * b[..., 2] - a[..., 2] * b[..., 1],
+                     a[..., 2] * b[..., 0] - a[..., 0] * b[..., 2],
+                     a[..., 0] * b[..., 1] - a[..., 1] * b[..., 0]], axis=-1)
+
+
+def affine_constants(A):
+    """Exact metrics of affine maps A (B, 3[d], 3[x]): J (B,), Ja (B, 3[i], 3[n])."""
+    ja = np.stack([_cross3(A[:, 1], A[:, 2]), _cross3(A[:, 2], A[:, 0]), _cross3(A[:, 0], A[:, 1])], axis=1)
+    jac = A[:, 0, 0] * ja[:, 0, 0] + A[:, 0, 1] * ja[:, 0, 1] + A[:, 0, 2] * ja[:, 0, 2]
+    return jac, ja
+
+
 def volume_metrics(ctrl, orders, family="LG", form="cross", index=-1):
     """Returns (jac (n1,n2,n3), ja (3, 3, n1,n2,n3) with ja[i, n] = Ja^i_n,
     sizes (3,))."""
@@ -91,6 +130,12 @@ def volume_metrics(ctrl, orders, family="LG", form="cross", index=-1):
                 ja[i, n] = -0.5 * curl_i
         av = tuple(np.stack([gX[c][k] for c in range(3)], axis=-1) for k in range(3))
         jac = np.einsum("ijkx,ijkx->ijk", av[0], np.cross(av[1], av[2]))
+        aff, A = affine_map(ctrl[None])
+        if aff[0]:
+            jc, jac_c = affine_constants(A)
+            ja = np.broadcast_to(jac_c[0][:, :, None, None, None], ja.shape).copy()
+            jac = np.full(jac.shape, jc[0])
+            av = tuple(np.broadcast_to(A[0, d], av[d].shape).copy() for d in range(3))
     else:
         raise ValueError(f"unknown metric form {form!r}")
     if np.min(jac) <= 0.0:
