@@ -116,3 +116,34 @@ def test_replica_timing_reduction_gloo():
     port = 29500 + (os.getpid() % 1000)
     mp.spawn(_replica_worker, args=(2, port, out), nprocs=2, join=True)
     assert dict(out) == {0: 3.0, 1: 3.0}
+
+
+def test_affine_metrics_are_exact_and_shared_with_the_oracle():
+    """Affine elements take exact constant curl-form metrics, by the same
+    element-wise rule in product and oracle (bit-identical); a jittered
+    (trilinear, non-parallelepiped) element keeps its collocated metrics."""
+    from oracle import geometry as og
+    from paper_1806_11456_b200 import geometry as pg
+
+    box = mesh.build_box(3, 2, 2, bounds=((0.0, 2 * np.pi), (0.0, 1.0), (-1.0, 3.0)))
+    jit = mesh.build_box(3, 2, 2, jitter=0.1, rng=np.random.default_rng(2))
+    assert pg.affine_map(box.nodes)[0].all() and not pg.affine_map(jit.nodes)[0].any()
+    for msh, affine in ((box, True), (jit, False)):
+        for fam in ("LGL", "LG"):
+            orders = (5, 3, 7)
+            jac, ja, _, _ = pg.volume_metrics(msh.nodes, orders, fam, "curl")
+            for e in range(msh.num_elements):
+                j2, a2, _ = og.volume_metrics(msh.nodes[e], orders, fam, "curl", e)
+                assert np.array_equal(j2, jac[e]) and np.array_equal(a2, ja[e])
+            flat = ja.reshape(len(ja), 9, -1)
+            spread = np.abs(flat - flat[:, :, :1]).max()
+            assert (spread == 0.0) == affine
+    # exact values: a box element of sides (hx, hy, hz) has J = hx hy hz / 8,
+    # Ja^i = (h_j h_k / 4) e_i
+    jac, ja, _, _ = pg.volume_metrics(box.nodes, (2, 2, 2), "LGL", "curl")
+    h = np.array([2 * np.pi / 3, 0.5, 2.0])
+    assert np.allclose(jac, np.prod(h) / 8, rtol=1e-15, atol=0)
+    for i in range(3):
+        j, k = (i + 1) % 3, (i + 2) % 3
+        assert np.allclose(ja[:, i, i], h[j] * h[k] / 4, rtol=1e-15, atol=0)
+        assert (ja[:, i, j] == 0).all() and (ja[:, i, k] == 0).all()
