@@ -311,7 +311,7 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st, boo
       const bool own = d.family == TDG_LGL && (isolated || d.nmface == 0);
       with_nx<LAW>(p->iso, [&](auto nx) -> int {
         if (own)
-          k_vol_lift_own<LAW, decltype(nx)::value><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q);
+          k_vol_lift_own<LAW, decltype(nx)::value><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q, coupled);
         else
           k_vol_lift<LAW, decltype(nx)::value><<<d.nwork, p->elem_threads, p->smem_lift, st>>>(d, Q, coupled);
         return 0;
@@ -516,6 +516,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     // (face_m_off, mortar_nodes, up and down of the descriptor are not read:
     // nonconforming faces are projected in registers by k_mortar)
     std::vector<int4> fdv(2 * static_cast<size_t>(desc->nfaces));
+    std::vector<int4> snb(6 * static_cast<size_t>(ns), make_int4(-1, 0, 0, 0));
     std::vector<int> cfv, mfv;
     for (int f = 0; f < desc->nfaces; ++f) {
       const int* fi = desc->face_info + 12 * f;
@@ -530,7 +531,16 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
       fdv[2 * f + 1] = make_int4(0, static_cast<int>(desc->side_off[kl]), static_cast<int>(desc->side_off[kr]),
                                  fi[5] | fi[6] << 3 | fi[7] << 6 | fi[8] << 9);
       (conf ? cfv : mfv).push_back(f);
+      if (conf) {
+        const int code = M1 | M2 << 3 | fi[4] << 6;
+        const int go = static_cast<int>(desc->face_geo_off[f]);
+        snb[kl] = make_int4(static_cast<int>(tl), go, code, 0);
+        snb[kr] = make_int4(static_cast<int>(tl), go, code | 1 << 9, 0);
+      }
     }
+    int4* snb_d = nullptr;
+    if (!rc && ns > 0) rc = p->mem.upload(snb.data(), snb.size(), &snb_d);
+    d.side_nb = snb_d;
     int *cf_d = nullptr, *mf_d = nullptr;
     if (!rc && !cfv.empty()) rc = p->mem.upload(cfv.data(), cfv.size(), &cf_d);
     if (!rc && !mfv.empty()) rc = p->mem.upload(mfv.data(), mfv.size(), &mf_d);
@@ -651,7 +661,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   const int NG = 3 * p->ngv;
   const size_t tn = static_cast<size_t>(desc->mtr_nodes);
   double *qtr, *lsurf = nullptr, *gtr = nullptr, *fsurf, *grad = nullptr;
-  double *qtrm = nullptr, *gtrm = nullptr;
+  double *qtrm = nullptr, *gtrm = nullptr, *gsf = nullptr;
   if (!rc) rc = p->mem.zeros(sn * p->nv, &qtr);
   if (!rc) rc = p->mem.zeros(tn * p->nv, &qtrm);
   if (!rc) rc = p->mem.zeros(sn * p->nv, &fsurf);
@@ -659,6 +669,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     if (!rc) rc = p->mem.zeros(sn * NG, &lsurf);
     if (!rc) rc = p->mem.zeros(sn * NG, &gtr);
     if (!rc) rc = p->mem.zeros(tn * NG, &gtrm);
+    if (!rc) rc = p->mem.zeros(sn * p->ngv, &gsf);
     if (!rc) rc = p->mem.zeros(static_cast<size_t>(p->nodes) * NG, &grad);
   }
   if (rc) {
@@ -676,6 +687,10 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     d.pf_face = knob("TDG_PF_FACE", 4);
     d.pf_down = knob("TDG_PF_DOWN", 5);
     d.div_mma = knob("TDG_DIV_MMA", 0);   // measured slower (extra barriers, serial directions); opt-in
+    // g* form of the conforming-face lift (plans served by k_vol_lift_own);
+    // TDG_GSTAR=0 restores the per-side g*·n σ arrays
+    d.gstar = (desc->family == TDG_LGL && p->viscous && d.ncface > 0 && d.nmface == 0 &&
+               knob("TDG_GSTAR", 1)) ? 1 : 0;
   }
   d.work = work_d;
   d.work_aff = work_aff_d;
@@ -690,6 +705,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.gtr = gtr;
   d.fsurf = fsurf;
   d.grad = grad;
+  d.gsf = gsf;
   // dynamic shared memory sized by the largest work item (<= MAXN nodes)
   const size_t mt = static_cast<size_t>(p->max_tot);
   p->smem_lift = static_cast<size_t>(std::max(p->ngv + 9, NG)) * mt * sizeof(double);

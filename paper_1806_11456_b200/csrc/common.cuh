@@ -82,6 +82,16 @@ struct DevPlan {
   double* gtr;    // [side_nodes][3*ngv] own-order gradient traces
   double* fsurf;  // [side_nodes][nv]      flux surface contributions
   double* grad;   // [nodes][3*ngv]        lifted gradient
+  // conforming-face lift in g* form (LGL plans without nonconforming faces):
+  // k_face<lift> writes g* = ½(g_L + g_R) once per face node ([ngv][nm] at
+  // the left side's trace offset) instead of g*·n σ for both sides (2 x 3 ngv),
+  // and k_vol_lift_own forms g*·n σ from it and the face geometry
+  int gstar;
+  double* gsf;    // [side_nodes][ngv] (left-side offsets used)
+  // per element side (slot*6+side) of a conforming interior face: x = the
+  // left side's trace offset (nodes; -1 otherwise), y = face-geometry
+  // offset, z = M1 | M2<<3 | orient<<6 | is_right<<9 (left frame)
+  const int4* side_nb;
 };
 
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {

@@ -110,6 +110,21 @@ __global__ void __launch_bounds__(FACE_THREADS_MAX) k_face(DevPlan P) {
   const int A = t % (M1 + 1), B = t / (M1 + 1);
   const int kR = right_index(A, B, M1, M2, orient);
   const long long tL = fd.x, tR = fd.y;
+  if (!FLUX && P.gstar) {
+    // g* form: one ½(g_L + g_R) per face node (the lift kernel applies n σ)
+    double ql[NV], qr[NV], gl[NGV], gr[NGV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      ql[v] = P.qtr[tL * NV + (long long)v * nm + t];
+      qr[v] = P.qtr[tR * NV + (long long)v * nm + kR];
+    }
+    L::grad_vars(P.prm, ql, gl);
+    L::grad_vars(P.prm, qr, gr);
+    double* dst = P.gsf + tL * NGV + t;
+#pragma unroll
+    for (int k = 0; k < NGV; ++k) dst[(long long)k * nm] = 0.5 * (gl[k] + gr[k]);
+    return;
+  }
   double val[COUT];
   face_point<LAW, FLUX>(P, P.qtr, P.gtr, tL, tR, nm, t, kR, P.face_geo + fd.w, val);
   double* dst = FLUX ? P.fsurf : P.lsurf;

@@ -119,6 +119,20 @@ __device__ __forceinline__ void prefetch_item_surface(const DevPlan& P, const do
   l2_prefetch_span(surf + s0 * C, static_cast<size_t>(s1 - s0) * C * sizeof(double));
 }
 
+// L2 bulk prefetch, one thread per element side, of the g* values and the
+// face geometry of every conforming interior side of a work item (g* form).
+template <int NGV>
+__device__ __forceinline__ void prefetch_item_gstar(const DevPlan& P, int2 wi, int N1, int N2, int N3) {
+  for (int u = threadIdx.x; u < wi.y * 6; u += blockDim.x) {
+    const int4 sn = P.side_nb[wi.x * 6 + u];
+    if (sn.x < 0) continue;
+    const int d = (u % 6) >> 1;
+    const int nf = d == 0 ? (N2 + 1) * (N3 + 1) : d == 1 ? (N1 + 1) * (N3 + 1) : (N1 + 1) * (N2 + 1);
+    l2_prefetch_span(P.gsf + (long long)sn.x * NGV, sizeof(double) * nf * NGV);
+    l2_prefetch_span(P.face_geo + sn.y, sizeof(double) * nf * 4);
+  }
+}
+
 // L2 bulk prefetch of a work item's per-node span of a C-component field
 // (the item's slots are contiguous), issued by thread ``who``.
 template <int C>
@@ -199,7 +213,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
 // BR1 lifted gradient at one node (operators.py:224-265): the volume part
 // −Σ_i WD_i(g Ja^i) from the staged g (and Ja on curved items), plus the
 // gathered surface contributions, times M⁻¹.  Shared by both lift kernels.
-template <int LAW, int NX>
+template <int LAW, int NX, bool GSTAR = false>
 __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T, const double* gs,
                                           const double* js, bool aff, int tot, int n, int n1p,
                                           int n2p, int n3p, int e, int node, int slot, int i, int j,
@@ -311,6 +325,39 @@ __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T,
     const int nf = np[a] * np[b];
     const int kf = ijk[a] + np[a] * ijk[b];
     const double lw = l * T.w[a][ijk[a]] * T.w[b][ijk[b]];
+    if (GSTAR) {
+      const int4 sn = P.side_nb[slot * 6 + s];
+      if (sn.x >= 0) {
+        // conforming interior side: g*·n σ from the face's g* (left frame)
+        // and the left side's σ, n; negated on the right side (exactly the
+        // values k_face<lift> would have stored for this side)
+        int tl = kf;
+        if ((sn.z >> 9) & 1) {
+          const int M1 = sn.z & 7, M2 = (sn.z >> 3) & 7, orient = (sn.z >> 6) & 7;
+          int ap, bp;
+          if (orient & 4) {
+            bp = kf % (M2 + 1);
+            ap = kf / (M2 + 1);
+          } else {
+            ap = kf % (M1 + 1);
+            bp = kf / (M1 + 1);
+          }
+          tl = ((orient & 1) ? M1 - ap : ap) + (M1 + 1) * ((orient & 2) ? M2 - bp : bp);
+        }
+        const double* gv = P.gsf + (long long)sn.x * NGV + tl;
+        const double* geo = P.face_geo + sn.y + tl;
+        const double sg = ((sn.z >> 9) & 1) ? -geo[0] : geo[0];
+        const double nrm[3] = {geo[nf], geo[2 * nf], geo[3 * nf]};
+        double g[NGV];
+#pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) g[kk] = gv[(long long)kk * nf];
+#pragma unroll
+        for (int d2 = 0; d2 < 3; ++d2)
+#pragma unroll
+          for (int kk = 0; kk < NGV; ++kk) acc[d2 * NGV + kk] += lw * (g[kk] * nrm[d2] * sg);
+        continue;
+      }
+    }
     const double* src = P.lsurf + P.side_off[slot * 6 + s] * NG + kf;
 #pragma unroll
     for (int c = 0; c < NG; ++c) acc[c] += lw * src[(long long)c * nf];
@@ -442,7 +489,8 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
 // values at a time (80 registers without spills, 3 blocks per SM: measured
 // faster than 4 blocks with spills at 64).
 template <int LAW, int NX>
-__global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, const double* __restrict__ Q) {
+__global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, const double* __restrict__ Q,
+                                                                   int coupled) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
@@ -454,7 +502,10 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
   const int n = n1p * n2p * n3p, tot = wi.y * n;
   double qa[NPT][NV];
   load_item_state<NV>(P, Q, wi, n, tot, qa);
-  prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+  if (coupled && P.gstar)
+    prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
+  else
+    prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
   load_tables(P, N1, N2, N3, T);
   const bool aff = P.work_aff[blockIdx.x] != 0;
   double* gs = sm;               // [NGV][tot]
@@ -470,7 +521,10 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
       const int e = t / n, node = t - e * n, slot = wi.x + e;
       const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
       double x[NG];
-      lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+      if (coupled && P.gstar)
+        lift_node<LAW, NX, true>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+      else
+        lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
       const long long gb = P.node_off[slot] * NG;
 #pragma unroll
       for (int c = 0; c < NG; ++c) P.grad[gb + (long long)c * n + node] = x[c];
