@@ -274,3 +274,48 @@ def test_host_batch_residual_matches_device_residual_and_oracle():
     Rh = fields.NodalField(op.orders, outs[2].cuda(), 5)
     assert (_to_oracle(Rh, of_o) - oo.residual(Qo)).norm_inf() <= RTOL * scale
     assert op.residual_host([]) == ([], [])
+
+
+@pytest.mark.parametrize("n_f", [7, 6, 5, 4, 3, 2])
+def test_line_transfer_kernel_is_bitwise_and_matches_oracle(n_f):
+    """Uniform isotropic 5-component level pairs run k_transfer_lines: bit for
+    bit the one-output-per-thread kernel (TDG_TRANSFER_LINES=0), and the
+    oracle's L2 projection / interpolation (multigrid.py:101-143) to 1e-13."""
+    import os
+
+    import torch
+
+    from oracle.fields import NodalField as ON
+    from oracle.fields import OrderField as OO
+    from oracle.multigrid import OrderTransfer as OT
+    from paper_1806_11456_b200 import fields, multigrid
+
+    nel = 12
+    of_f, of_c = fields.OrderField.uniform(nel, n_f), fields.OrderField.uniform(nel, n_f - 1)
+    os.environ["TDG_TRANSFER_LINES"] = "0"
+    try:
+        t_ref = multigrid.OrderTransfer(of_f, of_c, nv=5, family="LGL")
+    finally:
+        del os.environ["TDG_TRANSFER_LINES"]
+    t_lin = multigrid.OrderTransfer(of_f, of_c, nv=5, family="LGL")
+    g = torch.Generator(device="cuda").manual_seed(n_f)
+    rnd = lambda of: fields.NodalField(of, torch.rand(of.num_nodes * 5, dtype=torch.float64, device="cuda",
+                                                      generator=g) - 0.5, 5)
+    Qf, Qc, Qc0 = rnd(of_f), rnd(of_c), rnd(of_c)
+    assert torch.equal(t_lin.restrict(Qf).data, t_ref.restrict(Qf).data)
+    assert torch.equal(t_lin.prolong(Qc).data, t_ref.prolong(Qc).data)
+    a, b = Qf.copy(), Qf.copy()
+    t_lin.prolong_add(Qc, a, Qc0)
+    t_ref.prolong_add(Qc, b, Qc0)
+    assert torch.equal(a.data, b.data)
+    # oracle
+    oo_f, oo_c = OO(np.full((nel, 3), n_f)), OO(np.full((nel, 3), n_f - 1))
+    ot = OT(oo_f, oo_c, family="LGL")
+    of_o = ON(oo_f, Qf.to_oracle_blocks(), 5)
+    oc_o = ON(oo_c, Qc.to_oracle_blocks(), 5)
+    r_o = ot.restrict(of_o)
+    p_o = ot.prolong(oc_o)
+    r = ON(oo_c, t_lin.restrict(Qf).to_oracle_blocks(), 5)
+    p = ON(oo_f, t_lin.prolong(Qc).to_oracle_blocks(), 5)
+    assert (r - r_o).norm_inf() <= 1e-13 * max(r_o.norm_inf(), 1.0)
+    assert (p - p_o).norm_inf() <= 1e-13 * max(p_o.norm_inf(), 1.0)
