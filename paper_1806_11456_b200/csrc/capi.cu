@@ -525,8 +525,17 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
       const int kl = 6 * fi[0] + fi[1], kr = 6 * fi[2] + fi[3];
       const long long tl = conf ? desc->side_off[kl] : desc->side_info[4 * kl + 3];
       const long long tr = conf ? desc->side_off[kr] : desc->side_info[4 * kr + 3];
+      // uniform face geometry (every node's sigma and normal identical, e.g.
+      // a face of an affine element): the kernels read node 0's values
+      bool geo_const = true;
+      {
+        const int nmf = (M1 + 1) * (M2 + 1);
+        const double* gg = desc->face_geo + desc->face_geo_off[f];
+        for (int c = 0; c < 4 && geo_const; ++c)
+          for (int k = 1; k < nmf && geo_const; ++k) geo_const = gg[c * nmf + k] == gg[c * nmf];
+      }
       fdv[2 * f] = make_int4(static_cast<int>(tl), static_cast<int>(tr),
-                             M1 | M2 << 3 | fi[4] << 6 | (conf ? 1 : 0) << 9,
+                             M1 | M2 << 3 | fi[4] << 6 | (conf ? 1 : 0) << 9 | (geo_const ? 1 : 0) << 10,
                              static_cast<int>(desc->face_geo_off[f]));
       fdv[2 * f + 1] = make_int4(0, static_cast<int>(desc->side_off[kl]), static_cast<int>(desc->side_off[kr]),
                                  fi[5] | fi[6] << 3 | fi[7] << 6 | fi[8] << 9);
@@ -534,8 +543,8 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
       if (conf) {
         const int code = M1 | M2 << 3 | fi[4] << 6;
         const int go = static_cast<int>(desc->face_geo_off[f]);
-        snb[kl] = make_int4(static_cast<int>(tl), go, code, 0);
-        snb[kr] = make_int4(static_cast<int>(tl), go, code | 1 << 9, 0);
+        snb[kl] = make_int4(static_cast<int>(tl), go, code | (geo_const ? 1 : 0) << 10, 0);
+        snb[kr] = make_int4(static_cast<int>(tl), go, code | 1 << 9 | (geo_const ? 1 : 0) << 10, 0);
       }
     }
     int4* snb_d = nullptr;

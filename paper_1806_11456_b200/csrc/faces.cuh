@@ -33,11 +33,13 @@ template <int LAW, bool FLUX>
 __device__ __forceinline__ void face_point(const DevPlan& P, const double* qsrc, const double* gsrc,
                                            long long tL, long long tR, int nm, int t, int kR,
                                            const double* geo,
-                                           double* val /* [FLUX ? NV : 3 NGV] */) {
+                                           double* val /* [FLUX ? NV : 3 NGV] */,
+                                           bool gconst = false) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
-  const double sigma = geo[t];
-  const double nrm[3] = {geo[nm + t], geo[2 * nm + t], geo[3 * nm + t]};
+  const int tg = gconst ? 0 : t;   // uniform face geometry: node 0's values
+  const double sigma = geo[tg];
+  const double nrm[3] = {geo[nm + tg], geo[2 * nm + tg], geo[3 * nm + tg]};
   double ql[NV], qr[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
@@ -94,7 +96,7 @@ __global__ void __launch_bounds__(FACE_THREADS_MAX) k_face(DevPlan P) {
       const int mn = ((fn.z & 7) + 1) * (((fn.z >> 3) & 7) + 1);
       l2_prefetch_span(P.qtr + (long long)fn.x * NV, sizeof(double) * mn * NV);
       l2_prefetch_span(P.qtr + (long long)fn.y * NV, sizeof(double) * mn * NV);
-      l2_prefetch_span(P.face_geo + fn.w, sizeof(double) * mn * 4);
+      if (!((fn.z >> 10) & 1)) l2_prefetch_span(P.face_geo + fn.w, sizeof(double) * mn * 4);
       if (FLUX && L::viscous(P.prm)) {
         l2_prefetch_span(P.gtr + (long long)fn.x * NG, sizeof(double) * mn * NG);
         l2_prefetch_span(P.gtr + (long long)fn.y * NG, sizeof(double) * mn * NG);
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(FACE_THREADS_MAX) k_face(DevPlan P) {
     return;
   }
   double val[COUT];
-  face_point<LAW, FLUX>(P, P.qtr, P.gtr, tL, tR, nm, t, kR, P.face_geo + fd.w, val);
+  face_point<LAW, FLUX>(P, P.qtr, P.gtr, tL, tR, nm, t, kR, P.face_geo + fd.w, val, (fd.z >> 10) & 1);
   double* dst = FLUX ? P.fsurf : P.lsurf;
   const long long oL = tL * COUT;
   const long long oR = tR * COUT;

@@ -129,7 +129,7 @@ __device__ __forceinline__ void prefetch_item_gstar(const DevPlan& P, int2 wi, i
     const int d = (u % 6) >> 1;
     const int nf = d == 0 ? (N2 + 1) * (N3 + 1) : d == 1 ? (N1 + 1) * (N3 + 1) : (N1 + 1) * (N2 + 1);
     l2_prefetch_span(P.gsf + (long long)sn.x * NGV, sizeof(double) * nf * NGV);
-    l2_prefetch_span(P.face_geo + sn.y, sizeof(double) * nf * 4);
+    if (!((sn.z >> 10) & 1)) l2_prefetch_span(P.face_geo + sn.y, sizeof(double) * nf * 4);
   }
 }
 
@@ -345,7 +345,7 @@ __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T,
           tl = ((orient & 1) ? M1 - ap : ap) + (M1 + 1) * ((orient & 2) ? M2 - bp : bp);
         }
         const double* gv = P.gsf + (long long)sn.x * NGV + tl;
-        const double* geo = P.face_geo + sn.y + tl;
+        const double* geo = P.face_geo + sn.y + (((sn.z >> 10) & 1) ? 0 : tl);
         const double sg = ((sn.z >> 9) & 1) ? -geo[0] : geo[0];
         const double nrm[3] = {geo[nf], geo[2 * nf], geo[3 * nf]};
         double g[NGV];
