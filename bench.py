@@ -284,7 +284,7 @@ def run_b200(args):
     outs = [torch.empty_like(q0).pin_memory() for _ in range(nbuf)]
     Qh = [bufs[k % nbuf] for k in range(args.steps)]
     Rh = [outs[k % nbuf] for k in range(args.steps)]
-    op.residual_host(Qh[:2], out=Rh[:2])
+    op.residual_host(Qh[:nbuf], out=Rh[:nbuf])     # untimed: every staging buffer once
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -326,10 +326,34 @@ def run_b200(args):
                 torch.cuda.synchronize()
                 times.append(max_over_ranks(a.elapsed_time(b)))
         hist = [r["rnorm"] for r in solver.log if r["phase"] in ("post", "coarse") and r["level"] == len(solver.levels)]
+        # algorithmic HBM bytes of one pinned-sweep V-cycle (affine:
+        # m = 0): per level 6s fused RK stages (finest 480 B/node, coarse levels
+        # + 40 for the FAS source) and the other operator evaluations (finest 2,
+        # intermediate 3, coarsest 3c + 2 in all), one element_dt read (40
+        # B/node) per sweep, 160 (n_f + n_c) per level pair for the two
+        # restrictions and the prolong-add
+        sm = w4.smoother
+        nl = len(solver.levels)
+        vbytes = 0.0
+        for li, lev in enumerate(solver.levels):
+            n = lev.orders.num_nodes
+            src = 0 if li == nl - 1 else 40
+            if li == 0:
+                stages, evals, sweeps = 3 * sm["coarsest_sweeps"], 2, sm["coarsest_sweeps"]
+            else:
+                sweeps = sm["pre_sweeps"] + sm["post_sweeps"]
+                stages, evals = 3 * sweeps, (2 if li == nl - 1 else 3)
+            vbytes += n * (stages * (480 + src) + evals * (360 + src) + sweeps * 40)
+            if li > 0:
+                vbytes += 160 * (n + solver.levels[li - 1].orders.num_nodes)
+        vpeak, _ = _peak_hbm()
+        v_roof_ms = vbytes / (vpeak * 1e6)
         vcycle = {"config": w4.name, "levels": len(solver.levels), "ms_median": statistics.median(times),
                   "ms_all": [round(t, 3) for t in times], "fine_nodes": w4.orders.num_nodes,
                   "smoother": w4.smoother, "setup_s": round(setup4, 1),
-                  "rnorm_post": [float(x) for x in hist[-len(times):]]}
+                  "rnorm_post": [float(x) for x in hist[-len(times):]],
+                  "roofline": {"bound": "hbm", "algorithmic_gb": vbytes / 1e9, "peak": vpeak, "unit": "GB/s",
+                               "roofline_ms": v_roof_ms, "frac": v_roof_ms / statistics.median(times)}}
         del solver
 
     # small configs: V-cycle latency (CUDA-graph replay of pinned-sweep cycles)
