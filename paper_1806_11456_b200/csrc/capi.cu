@@ -696,6 +696,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     d.pf_face = knob("TDG_PF_FACE", 4);
     d.pf_down = knob("TDG_PF_DOWN", 5);
     d.div_mma = knob("TDG_DIV_MMA", 0);   // measured slower (extra barriers, serial directions); opt-in
+    d.pf_item = knob("TDG_PF_ITEM", 1);
     // g* form of the conforming-face lift (plans served by k_vol_lift_own);
     // TDG_GSTAR=0 restores the per-side g*·n σ arrays
     d.gstar = (desc->family == TDG_LGL && p->viscous && d.ncface > 0 && d.nmface == 0 &&

@@ -53,6 +53,7 @@ struct DevPlan {
   int nsm;        // SMs: kernels prefetch the work about one wave ahead (L2)
   int pf_trace, pf_face, pf_down;   // look-ahead distances, blocks per SM
   int div_mma;    // weak divergence of the flux kernel on the FP64 tensor cores
+  int pf_item;    // flux kernel: L2 bulk prefetch of the item's Q and grad spans
   // side work items for side kernels: (slot, side | kind<<8), ghost offset
   int nside_iso;
   const int4* side_iso;      // isolated: every side of every element

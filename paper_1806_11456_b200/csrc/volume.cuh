@@ -143,6 +143,14 @@ __device__ __forceinline__ void prefetch_item_nodes(const DevPlan& P, const doub
   l2_prefetch_span(x + n0 * C, static_cast<size_t>(n1 - n0) * C * sizeof(double));
 }
 
+// L2 bulk prefetch of a curved work item's per-node metrics ([10][n] per
+// slot, contiguous over the item's slots), issued by thread ``who``.
+__device__ __forceinline__ void prefetch_item_metrics(const DevPlan& P, int2 wi, int n, int who) {
+  if (threadIdx.x != who || P.work_aff[blockIdx.x]) return;
+  const long long m0 = P.metric_off[wi.x], m1 = P.metric_off[wi.x + wi.y - 1] + 10LL * n;
+  l2_prefetch_span(P.metrics + m0, static_cast<size_t>(m1 - m0) * sizeof(double));
+}
+
 // The work item per_sm * nsm blocks ahead of this block (blocks start in
 // index order: with per_sm resident blocks per SM it runs about one wave
 // later), or wi.y == 0 if none.
@@ -436,6 +444,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
   double qa[NPT][NV];
   load_item_state<NV>(P, Q, wi, n, tot, qa);
   prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+  if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
   load_tables(P, N1, N2, N3, T);
   const bool aff = P.work_aff[blockIdx.x] != 0;
   double* gs = sm;               // [NGV][tot]
@@ -506,6 +515,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
     prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
   else
     prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+  if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
   load_tables(P, N1, N2, N3, T);
   const bool aff = P.work_aff[blockIdx.x] != 0;
   double* gs = sm;               // [NGV][tot]
@@ -640,6 +650,13 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   // epilogue inputs, read after the contraction
   if (MODE != MODE_F) prefetch_item_nodes<NV>(P, MODE == MODE_A ? A.X : A.S, wi, 32);
   if (MODE == MODE_RK && A.stage != 0) prefetch_item_nodes<NV>(P, A.W, wi, 64);
+  if (P.pf_item) {
+    // the item's state and gradient spans, read node by node below (the
+    // second node of each thread only after the first one's flux)
+    prefetch_item_nodes<NV>(P, Q, wi, 96);
+    if (L::viscous(P.prm)) prefetch_item_nodes<NG>(P, P.grad, wi, 128);
+    prefetch_item_metrics(P, wi, (N1 + 1) * (N2 + 1) * (N3 + 1), 160);
+  }
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
   const bool visc = L::viscous(P.prm);
