@@ -657,11 +657,16 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     for (int e = 0; e < work[k].y; ++e) a &= desc->affine[work[k].x + e] != 0;
     work_aff[k] = a;
   }
+  std::vector<int> work_ord(3 * work.size());
+  for (size_t k = 0; k < work.size(); ++k)
+    for (int dd = 0; dd < 3; ++dd) work_ord[3 * k + dd] = p->orders_h[3 * work[k].x + dd];
   int2* work_d;
   int* work_aff_d = nullptr;
+  int* work_ord_d = nullptr;
   int4 *iso_d, *bnd_d;
   rc = p->mem.upload(work.data(), work.size(), &work_d);
   if (!rc) rc = p->mem.upload(work_aff.data(), work_aff.size(), &work_aff_d);
+  if (!rc) rc = p->mem.upload(work_ord.data(), work_ord.size(), &work_ord_d);
   if (!rc) rc = p->mem.upload(iso.data(), iso.size(), &iso_d);
   if (!rc) rc = p->mem.upload(bnd.data(), bnd.size(), &bnd_d);
   const size_t sn = static_cast<size_t>(desc->side_nodes);
@@ -704,6 +709,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   }
   d.work = work_d;
   d.work_aff = work_aff_d;
+  d.work_ord = work_ord_d;
   d.nside_iso = static_cast<int>(iso.size());
   d.side_iso = iso_d;
   d.nside_bnd = static_cast<int>(bnd.size());

@@ -50,6 +50,7 @@ struct DevPlan {
   int nwork;
   const int2* work;
   const int* work_aff;   // per work item: 1 if every element of the item is affine
+  const int* work_ord;   // per work item: its (N1, N2, N3), read without waiting for work[]
   int nsm;        // SMs: kernels prefetch the work about one wave ahead (L2)
   int pf_trace, pf_face, pf_down;   // look-ahead distances, blocks per SM
   int div_mma;    // weak divergence of the flux kernel on the FP64 tensor cores

@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
     const int2 wn = item_ahead(P, P.pf_trace);
     if (wn.y > 0) prefetch_item_nodes<NV>(P, Q, wn, 0);
   }
-  const int* od = P.orders + 3 * wi.x;
+  const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int No[3] = {od[0], od[1], od[2]};
   for (int u = threadIdx.x; u < 48; u += blockDim.x)
     sb[u / 16][u % 16] = P.tables[OFF_BND + No[u / 16] * 16 + (u % 16)];
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
   __shared__ ElemTables T;
   extern __shared__ double sm[];
   const int2 wi = P.work[blockIdx.x];
-  const int* od = P.orders + 3 * wi.x;
+  const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
   __shared__ ElemTables T;
   extern __shared__ double sm[];
   const int2 wi = P.work[blockIdx.x];
-  const int* od = P.orders + 3 * wi.x;
+  const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   __shared__ ElemTables T;
   extern __shared__ double sm[];
   const int2 wi = P.work[blockIdx.x];
-  const int* od = P.orders + 3 * wi.x;
+  const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
   prefetch_item_surface<NV>(P, P.fsurf, wi, N1, N2);
   // epilogue inputs, read after the contraction
@@ -854,7 +854,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_element_dt(DevPlan P, const do
   constexpr int NV = L::NV;
   __shared__ unsigned long long smax[64];
   const int2 wi = P.work[blockIdx.x];
-  const int* od = P.orders + 3 * wi.x;
+  const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int No[3] = {od[0], od[1], od[2]};
   const int n = (No[0] + 1) * (No[1] + 1) * (No[2] + 1), tot = wi.y * n;
   for (int u = threadIdx.x; u < 64; u += blockDim.x) smax[u] = 0ull;
@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_norm(DevPlan P, const double* 
   __shared__ unsigned long long emax[64];
   __shared__ double red[32];
   const int2 wi = P.work[blockIdx.x];
-  const int* od = P.orders + 3 * wi.x;
+  const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int n = (od[0] + 1) * (od[1] + 1) * (od[2] + 1), tot = wi.y * n;
   for (int u = threadIdx.x; u < 64; u += blockDim.x) emax[u] = 0ull;
   __syncthreads();
