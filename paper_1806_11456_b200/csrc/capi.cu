@@ -294,9 +294,9 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st, boo
         // (timer class TDG_K_DOWN = "mortar_face")
         KTimer kd(TDG_K_DOWN, st);
         if (flux)
-          k_mortar<LAW, true><<<(d.nmface + 3) / 4, 128, 0, st>>>(d);
+          k_mortar<LAW, true><<<(d.nmface + MORTAR_WARPS - 1) / MORTAR_WARPS, 32 * MORTAR_WARPS, 0, st>>>(d);
         else
-          k_mortar<LAW, false><<<(d.nmface + 3) / 4, 128, 0, st>>>(d);
+          k_mortar<LAW, false><<<(d.nmface + MORTAR_WARPS - 1) / MORTAR_WARPS, 32 * MORTAR_WARPS, 0, st>>>(d);
         LAUNCH_CHECK("k_mortar");
       }
     }
