@@ -147,6 +147,7 @@ struct tdg_plan {
   size_t smem_lift = 0, smem_flux = 0;
   int elem_threads = ELEM_THREADS;   // block size of the lift / flux kernels
   int max_tot = MAXN;                // largest work item (nodes)
+  int trace_threads = ELEM_THREADS;  // k_trace_q block size
   int64_t side_nodes = 0;
   int iso = -1;          // isotropic order of a single-bucket plan, else -1
   bool tma = false;      // persistent TMA-pipelined flux kernel (TDG_TMA=1 enables)
@@ -263,7 +264,7 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st, boo
   const int coupled = isolated ? 0 : 1;
   if (!traces_fresh) {
     KTimer kt(TDG_K_TRACE, st);
-    k_trace_q<L::NV><<<d.nwork, ELEM_THREADS, 0, st>>>(d, Q, coupled);
+    k_trace_q<L::NV><<<d.nwork, p->trace_threads, 0, st>>>(d, Q, coupled);
     LAUNCH_CHECK("k_trace_q");
   }
   p->traces_of = Q;
@@ -702,6 +703,11 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     d.pf_down = knob("TDG_PF_DOWN", 5);
     d.div_mma = knob("TDG_DIV_MMA", 0);   // measured slower (extra barriers, serial directions); opt-in
     d.pf_item = knob("TDG_PF_ITEM", 1);
+    // own-order trace branch (no mortars): 128-thread blocks split an N=7
+    // element's 384 face nodes into three full rounds (256: one full, one
+    // half-empty); measured config 4 N=7 0.127 -> 0.097 ms.  Mortar plans
+    // keep 256 (warp per side; 192 / 128 measured slower)
+    p->trace_threads = knob("TDG_TRACE_THREADS", d.nmface == 0 ? 128 : ELEM_THREADS);
     // g* form of the conforming-face lift (plans served by k_vol_lift_own);
     // TDG_GSTAR=0 restores the per-side g*·n σ arrays
     d.gstar = (desc->family == TDG_LGL && p->viscous && d.ncface > 0 && d.nmface == 0 &&
