@@ -370,7 +370,8 @@ bool launch_transfer_iso(const tdg_transfer* t, int ns, int nd, const double* in
                          double* out, cudaStream_t st) {
   if (ns != NS || nd != ND) return false;
   if (t->lines)
-    k_transfer_lines<MODE, 5, NS, ND><<<t->nwork, ELEM_THREADS, t->smem, st>>>(t->d, in, in2, out);
+    k_transfer_lines<MODE, 5, NS, ND><<<t->nwork, transfer_lines_threads<NS, ND>(), t->smem, st>>>(t->d, in, in2,
+                                                                                                  out);
   else
     k_transfer<MODE, 5, NS, ND><<<t->nwork, ELEM_THREADS, t->smem, st>>>(t->d, in, in2, out);
   return true;

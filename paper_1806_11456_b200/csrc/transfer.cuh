@@ -129,8 +129,16 @@ constexpr int kTransferUnroll = TDG_TRANSFER_UNROLL;
 // Q_c - Q_c0 formed on the fly); each pass is one 1D line per thread, held in
 // registers (NS loads -> ND outputs), instead of one output per thread
 // re-reading the line.  Same per-output summation order as k_transfer.
+// Block size: the N=7 <-> 6 pairs (one element per item) have 320, 280 and
+// 245 lines in their three passes, so 320 threads run each pass in one round
+// (256 need two rounds for two of them); other pairs use 256.
+template <int NS, int ND>
+__host__ __device__ constexpr int transfer_lines_threads() { return (NS == 8 || ND == 8) ? 320 : ELEM_THREADS; }
+
 template <int MODE, int NVC, int NS, int ND>
-__global__ void __launch_bounds__(ELEM_THREADS, TDG_TRANSFER_BLOCKS) k_transfer_lines(DevTransfer T, const double* __restrict__ in,
+__global__ void __launch_bounds__(transfer_lines_threads<NS, ND>(),
+                                  TDG_TRANSFER_BLOCKS * ELEM_THREADS / transfer_lines_threads<NS, ND>())
+    k_transfer_lines(DevTransfer T, const double* __restrict__ in,
                                                                  const double* __restrict__ in2,
                                                                  double* __restrict__ out) {
   extern __shared__ double sm[];
@@ -139,7 +147,8 @@ __global__ void __launch_bounds__(ELEM_THREADS, TDG_TRANSFER_BLOCKS) k_transfer_
   constexpr int ns = NS * NS * NS, nd = ND * ND * ND;
   constexpr int S1 = ND * NS * NS, S2 = ND * ND * NS;
   constexpr int MA = ns > S2 ? ns : S2, MB = S1;
-  constexpr int R = (MAXN * NVC + ELEM_THREADS - 1) / ELEM_THREADS;
+  constexpr int NT = transfer_lines_threads<NS, ND>();
+  constexpr int R = (MAXN * NVC + NT - 1) / NT;
   const int2 wi = T.work[blockIdx.x];
   const int fs0 = wi.x, E = wi.y;
   const int cs0 = T.c_slot_of_f[fs0];
@@ -150,7 +159,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, TDG_TRANSFER_BLOCKS) k_transfer_
   double x[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int u = threadIdx.x + r * ELEM_THREADS;
+    const int u = threadIdx.x + r * NT;
     if (u < tot) {
       x[r] = in[ib + u];
       if (MODE == TR_PROLONG_ADD && in2) x[r] -= in2[ib + u];
@@ -162,7 +171,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, TDG_TRANSFER_BLOCKS) k_transfer_
   double* B = sm + E * NVC * MA;       // [E*NVC][MB]
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int u = threadIdx.x + r * ELEM_THREADS;
+    const int u = threadIdx.x + r * NT;
     if (u < tot) A[(u / ns) * MA + u % ns] = x[r];
   }
   __syncthreads();
