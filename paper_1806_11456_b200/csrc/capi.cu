@@ -708,7 +708,14 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     // element's 384 face nodes into three full rounds (256: one full, one
     // half-empty); measured config 4 N=7 0.127 -> 0.097 ms.  Mortar plans
     // keep 256 (warp per side; 192 / 128 measured slower)
-    p->trace_threads = knob("TDG_TRACE_THREADS", d.nmface == 0 ? 128 : ELEM_THREADS);
+    // (items with many small elements, > 700 face nodes, keep 256: measured
+    // on config-4 levels N = 1, 2)
+    int tasks = 0;
+    for (const int2& w : work) {
+      const int* o = &p->orders_h[3 * w.x];
+      tasks = std::max(tasks, w.y * 2 * ((o[1] + 1) * (o[2] + 1) + (o[0] + 1) * (o[2] + 1) + (o[0] + 1) * (o[1] + 1)));
+    }
+    p->trace_threads = knob("TDG_TRACE_THREADS", d.nmface == 0 && tasks <= 700 ? 128 : ELEM_THREADS);
     // g* form of the conforming-face lift (plans served by k_vol_lift_own);
     // TDG_GSTAR=0 restores the per-side g*·n σ arrays
     d.gstar = (desc->family == TDG_LGL && p->viscous && d.ncface > 0 && d.nmface == 0 &&
