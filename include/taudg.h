@@ -91,16 +91,6 @@ typedef struct {
    * w = offset (nodes) of the side's mortar-order traces when nonconforming */
   const int32_t* side_info;    /* [nslots*6*4] */
   int64_t mtr_nodes;           /* total mortar-trace nodes of nonconforming sides */
-  /* Reserved (ABI-stable, not read since nonconforming faces are projected
-     in registers, one warp per face): mortar-array offsets and the up / down
-     projection task lists.  Callers may pass zeros / NULL. */
-  const int64_t* face_m_off;   /* [nfaces] mortar-array offset (nodes), -1 when conforming */
-  int64_t mortar_nodes;        /* total mortar nodes of nonconforming faces */
-  int32_t nup;                 /* up-projection tasks */
-  const int32_t* up;           /* [nup*2] (slot, side) */
-  int32_t ndown;               /* down-projection tasks */
-  const int32_t* down;         /* [ndown*2] (face, is_right) */
-
   int32_t nbfaces;             /* boundary faces */
   const int32_t* bface_info;   /* [nbfaces*4] slot, side, bc kind, 0 */
   const int64_t* ghost_off;    /* [nbfaces] offset (doubles) into ghost, [nv][nf] */
@@ -150,6 +140,12 @@ int tdg_residual_host(tdg_plan* plan, int32_t nbatch, const double* const* Q_hos
 int tdg_tau(tdg_plan* plan, const double* Q, const double* S_pde, double* tau_dev,
             int isolated, void* stream);
 
+/* DGOperator.truncation_from_avalue (operators.py:355-360), coupled tau of
+ * tau.recorder_for (tau.py:178): tau_dev[elem_id] = max over nodes and
+ * unknowns of |M (S_pde - A)| for a given A (device field).  S nullable
+ * (zero).  Every element is written (no reset needed). */
+int tdg_tau_from_avalue(tdg_plan* plan, const double* A, const double* S_pde, double* tau_dev,
+                        void* stream);
 /* timestep.element_dt / compute_dt (timestep.py:40-80):
  * dt_slot[slot] = min_d min(C_a h_d/(s_max max(N_d,1)^2), C_nu h_d^2/(mu max(N_d,1)^4));
  * dt_min_dev (nullable) = min over elements (reset inside). */
@@ -208,10 +204,15 @@ int tdg_prolong(const tdg_transfer* t, const double* coarse, double* fine, void*
 int tdg_prolong_add(const tdg_transfer* t, const double* Qc, const double* Qc0, double* fine,
                     void* stream);
 
-/* Lifted BR1 gradient of the last evaluation (debug/parity): copies the
- * plan's gradient buffer [3][ngv][n] per element to dst (device). */
-int tdg_copy_gradient(tdg_plan* plan, double* dst, void* stream);
-
+/* Lifted BR1 gradient (operators.py:224-265; debug/parity): one trace + lift
+ * pass over Q (coupled or isolated) that writes the per-node gradient,
+ * [3][ngv][n] per element in slot order, to dst (device).  Plans whose flux
+ * kernel recomputes the gradient never store it during evaluations. */
+int tdg_gradient(tdg_plan* plan, const double* Q, int isolated, double* dst, void* stream);
+/* Plan facts for tests and the bench: recompute = 1 when the flux kernel
+ * recomputes the BR1 gradient (every work item affine); nwork = element work
+ * items (blocks per element-kernel launch). */
+int tdg_plan_info(const tdg_plan* plan, int32_t* recompute, int32_t* nwork);
 /* Debug/parity: copy a face scratch buffer of the last evaluation to dst
  * (device): which = 0 Q traces [nv], 1 lift surface [3 ngv], 2 gradient
  * traces [3 ngv], 3 flux surface [nv]; per element side at side_off*C as

@@ -29,8 +29,7 @@ class PlanDesc(C.Structure):
         ("side_off", _pi64), ("side_nodes", _i64), ("side_geo", _pd),
         ("nfaces", _i32), ("face_info", _pi32), ("face_geo_off", _pi64), ("face_geo", _pd),
         ("face_geo_len", _i64),
-        ("side_info", _pi32), ("mtr_nodes", _i64), ("face_m_off", _pi64),
-        ("mortar_nodes", _i64), ("nup", _i32), ("up", _pi32), ("ndown", _i32), ("down", _pi32),
+        ("side_info", _pi32), ("mtr_nodes", _i64),
         ("nbfaces", _i32), ("bface_info", _pi32), ("ghost_off", _pi64), ("ghost", _pd),
         ("ghost_len", _i64),
     ]
@@ -64,7 +63,9 @@ SIGNATURES = {
     "tdg_restrict": ([_VP, _VP, _VP, _VP], C.c_int),
     "tdg_prolong": ([_VP, _VP, _VP, _VP], C.c_int),
     "tdg_prolong_add": ([_VP, _VP, _VP, _VP, _VP], C.c_int),
-    "tdg_copy_gradient": ([_VP, _VP, _VP], C.c_int),
+    "tdg_gradient": ([_VP, _VP, C.c_int, _VP, _VP], C.c_int),
+    "tdg_plan_info": ([_VP, _pi32, _pi32], C.c_int),
+    "tdg_tau_from_avalue": ([_VP, _VP, _VP, _VP, _VP], C.c_int),
     "tdg_debug_copy": ([_VP, C.c_int, _VP, _pi64, _VP], C.c_int),
     "tdg_timing_enable": ([C.c_int], C.c_int),
     "tdg_timing_read": ([_pd, _pi64, C.c_int], C.c_int),

@@ -21,7 +21,6 @@
 #include "laws.cuh"
 #include "transfer.cuh"
 #include "volume.cuh"
-#include "volume_tma.cuh"
 
 using namespace tdg;
 
@@ -143,16 +142,15 @@ struct tdg_plan {
   // (set by evaluations; an RK stage leaves the traces of its new state only
   // when its epilogue wrote them)
   const double* traces_of = nullptr;
-  bool rk_traces = false;   // LGL, no nonconforming face, no TMA kernel
+  bool rk_traces = false;   // LGL, no nonconforming face
   size_t smem_lift = 0, smem_flux = 0;
   int elem_threads = ELEM_THREADS;   // block size of the lift / flux kernels
   int max_tot = MAXN;                // largest work item (nodes)
   int trace_threads = ELEM_THREADS;  // k_trace_q block size
   int64_t side_nodes = 0;
   int iso = -1;          // isotropic order of a single-bucket plan, else -1
-  bool tma = false;      // persistent TMA-pipelined flux kernel (TDG_TMA=1 enables)
   int nsm = 148;
-  size_t smem_flux_tma = 0;
+  double* grad_dbg = nullptr;   // gradient buffer for tdg_gradient on recompute plans (lazy)
   // host-buffer batch evaluation (tdg_residual_host): two device staging
   // slots, two copy streams, per-slot events; created on first use
   struct Staging {
@@ -236,30 +234,32 @@ int setup_attrs(tdg_plan* p) {
     constexpr int NX = decltype(nx)::value;
     int r;
     if ((r = allow_smem(k_vol_lift<LAW, NX>, lift))) return r;
-    if ((r = allow_smem(k_vol_lift_own<LAW, NX>, own))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX>, flux))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX>, flux))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX>, flux))) return r;
+    if ((r = allow_smem(k_vol_lift_own<LAW, NX, false>, own))) return r;
+    if ((r = allow_smem(k_vol_lift_own<LAW, NX, true>, own))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX, false>, flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX, false>, flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX, false>, flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX, true>, flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX, true>, flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX, true>, flux))) return r;
     return TDG_OK;
   });
   if (rc) return rc;
-  // cold modes and the opt-in TMA kernel use runtime orders only
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, -1>, flux))) return rc;
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, -1>, flux))) return rc;
-  const size_t tb = p->smem_flux_tma;
-  if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_F, -1>, tb))) return rc;
-  if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_A, -1>, tb))) return rc;
-  if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_R, -1>, tb))) return rc;
-  if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_RK, -1>, tb))) return rc;
-  if ((rc = allow_smem(k_vol_flux_tma<LAW, MODE_TAU, -1>, tb))) return rc;
+  // cold modes use runtime orders only
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, -1, false>, flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, -1, false>, flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, -1, true>, flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, -1, true>, flux))) return rc;
   return TDG_OK;
 }
 
-// trace -> lift (if viscous) -> face fluxes; leaves fsurf ready for k_vol_flux
+// trace -> lift (if viscous) -> face fluxes; leaves fsurf ready for k_vol_flux.
+// ``d`` is the plan's device view (tdg_gradient passes a copy that stores the
+// per-node gradient); lift_only stops after the lift.
 template <int LAW>
-int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st, bool traces_fresh = false) {
+int run_surface(tdg_plan* p, const DevPlan& d, const double* Q, int isolated, cudaStream_t st,
+                bool traces_fresh = false, bool lift_only = false) {
   using L = Law<LAW>;
-  const DevPlan& d = p->d;
   if (d.nwork == 0) return TDG_OK;
   const int coupled = isolated ? 0 : 1;
   if (!traces_fresh) {
@@ -309,39 +309,53 @@ int run_surface(tdg_plan* p, const double* Q, int isolated, cudaStream_t st, boo
     {
       KTimer kt(TDG_K_VOL_LIFT, st);
       // LGL and every evaluated side on own-order traces: direct trace writes
+      // (face nodes only when the flux kernel recomputes the gradient)
       const bool own = d.family == TDG_LGL && (isolated || d.nmface == 0);
+      const bool face_only = d.recompute && d.grad == nullptr;
       with_nx<LAW>(p->iso, [&](auto nx) -> int {
-        if (own)
-          k_vol_lift_own<LAW, decltype(nx)::value><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q, coupled);
+        constexpr int NX = decltype(nx)::value;
+        if (own && face_only)
+          k_vol_lift_own<LAW, NX, true><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q, coupled);
+        else if (own)
+          k_vol_lift_own<LAW, NX, false><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q, coupled);
         else
-          k_vol_lift<LAW, decltype(nx)::value><<<d.nwork, p->elem_threads, p->smem_lift, st>>>(d, Q, coupled);
+          k_vol_lift<LAW, NX><<<d.nwork, p->elem_threads, p->smem_lift, st>>>(d, Q, coupled);
         return 0;
       });
     }
     LAUNCH_CHECK("k_vol_lift");
   }
+  if (lift_only) return TDG_OK;
   return sides(true);
 }
 
 template <int LAW, int MODE>
-int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a, cudaStream_t st,
+int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a0, cudaStream_t st,
              bool traces_fresh = false) {
-  int rc = run_surface<LAW>(p, Q, isolated, st, traces_fresh);
+  int rc = run_surface<LAW>(p, p->d, Q, isolated, st, traces_fresh);
   if (rc) return rc;
   if (p->d.nwork == 0) return TDG_OK;
+  FluxArgs a = a0;
+  a.coupled = isolated ? 0 : 1;
   {
     KTimer kt(TDG_K_VOL_FLUX, st);
     constexpr bool hot = MODE == MODE_R || MODE == MODE_RK || MODE == MODE_A;
-    if (p->tma) {
-      const int grid = std::min(p->d.nwork, p->nsm);
-      k_vol_flux_tma<LAW, MODE, -1><<<grid, TMA_THREADS, p->smem_flux_tma, st>>>(p->d, Q, a);
-    } else if (hot) {
+    const bool rec = p->d.recompute != 0;
+    auto launch = [&](auto nx, auto recv) {
+      constexpr int NX = decltype(nx)::value;
+      constexpr bool REC = decltype(recv)::value;
+      k_vol_flux<LAW, MODE, NX, REC><<<p->d.nwork, p->elem_threads, p->smem_flux, st>>>(p->d, Q, a);
+      return 0;
+    };
+    if (hot) {
       with_nx<LAW>(p->iso, [&](auto nx) -> int {
-        k_vol_flux<LAW, MODE, hot ? decltype(nx)::value : -1><<<p->d.nwork, p->elem_threads, p->smem_flux, st>>>(p->d, Q, a);
-        return 0;
+        constexpr int NX = hot ? decltype(nx)::value : -1;
+        return rec ? launch(std::integral_constant<int, NX>(), std::true_type())
+                   : launch(std::integral_constant<int, NX>(), std::false_type());
       });
     } else {
-      k_vol_flux<LAW, MODE, -1><<<p->d.nwork, p->elem_threads, p->smem_flux, st>>>(p->d, Q, a);
+      rec ? launch(std::integral_constant<int, -1>(), std::true_type())
+          : launch(std::integral_constant<int, -1>(), std::false_type());
     }
   }
   LAUNCH_CHECK("k_vol_flux");
@@ -515,8 +529,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   UP(side_info_i, desc->side_info, 4 * 6 * ns);
   {
     // packed per-face descriptors and the conforming / nonconforming face lists
-    // (face_m_off, mortar_nodes, up and down of the descriptor are not read:
-    // nonconforming faces are projected in registers by k_mortar)
+    // (nonconforming faces are projected in registers by k_mortar)
     std::vector<int4> fdv(2 * static_cast<size_t>(desc->nfaces));
     std::vector<int4> snb(6 * static_cast<size_t>(ns), make_int4(-1, 0, 0, 0));
     std::vector<int> cfv, mfv;
@@ -626,7 +639,9 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   for (int s = 0; s < ns;) {
     const int* o = &p->orders_h[3 * s];
     const int n = (o[0] + 1) * (o[1] + 1) * (o[2] + 1);
-    const int cap = std::max(1, static_cast<int>(item_nodes / n));
+    // <= MAX_ITEM_ELEMS elements: per-element reductions (tau, dt, norms)
+    // use fixed shared-memory arrays of that size
+    const int cap = std::min(MAX_ITEM_ELEMS, std::max(1, static_cast<int>(item_nodes / n)));
     int e = s;
     while (e < ns && e - s < cap && p->orders_h[3 * e] == o[0] && p->orders_h[3 * e + 1] == o[1] &&
            p->orders_h[3 * e + 2] == o[2])
@@ -686,7 +701,6 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     if (!rc) rc = p->mem.zeros(sn * NG, &gtr);
     if (!rc) rc = p->mem.zeros(tn * NG, &gtrm);
     if (!rc) rc = p->mem.zeros(sn * p->ngv, &gsf);
-    if (!rc) rc = p->mem.zeros(static_cast<size_t>(p->nodes) * NG, &grad);
   }
   if (rc) {
     delete p;
@@ -702,8 +716,21 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     d.pf_trace = knob("TDG_PF_TRACE", 2);
     d.pf_face = knob("TDG_PF_FACE", 4);
     d.pf_down = knob("TDG_PF_DOWN", 5);
-    d.div_mma = knob("TDG_DIV_MMA", 0);   // measured slower (extra barriers, serial directions); opt-in
     d.pf_item = knob("TDG_PF_ITEM", 1);
+    // every work item affine: the flux kernel recomputes the BR1 gradient and
+    // the lift writes only its side traces.  Opt-in (TDG_RECOMPUTE=1): measured
+    // slower on config 4 (V-cycle 60.5 -> 74-80 ms), the element kernels are
+    // shared-memory-bandwidth bound and the recompute adds 96 loads per node
+    bool all_aff = !work.empty();
+    for (int a : work_aff) all_aff = all_aff && a != 0;
+    d.recompute = (p->viscous && all_aff && knob("TDG_RECOMPUTE", 0)) ? 1 : 0;
+    int coll = 0;
+    for (int dd = 0; dd < 3; ++dd) {
+      bool c = ns > 0;
+      for (int s = 0; s < ns && c; ++s) c = p->orders_h[3 * s + dd] == 0;
+      coll |= c ? 1 << dd : 0;
+    }
+    d.collapsed = coll;
     // own-order trace branch (no mortars): 128-thread blocks split an N=7
     // element's 384 face nodes into three full rounds (256: one full, one
     // half-empty); measured config 4 N=7 0.127 -> 0.097 ms.  Mortar plans
@@ -734,7 +761,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.lsurf = lsurf;
   d.gtr = gtr;
   d.fsurf = fsurf;
-  d.grad = grad;
+  d.grad = nullptr;
   d.gsf = gsf;
   // dynamic shared memory sized by the largest work item (<= MAXN nodes)
   const size_t mt = static_cast<size_t>(p->max_tot);
@@ -745,14 +772,15 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     p->smem_lift_own = static_cast<size_t>(p->ngv + (curved ? 9 : 0)) * mt * sizeof(double);
   }
   p->smem_flux = static_cast<size_t>(3 * p->nv) * mt * sizeof(double);
-  p->smem_flux_tma = static_cast<size_t>(p->nv == 5 ? tma_flux_smem_doubles<5, 12>()
-                                                    : tma_flux_smem_doubles<1, 3>()) * sizeof(double);
+  if (p->viscous && !d.recompute) {
+    if ((rc = p->mem.zeros(static_cast<size_t>(p->nodes) * NG, &grad))) {
+      delete p;
+      return rc;
+    }
+    d.grad = grad;
+  }
   {
-    // measured slower than the 3-blocks/SM kernel at one block per SM
-    // (compute-phase latency dominates once loads are decoupled); opt-in
-    const char* env = getenv("TDG_TMA");
-    p->tma = env && env[0] == '1';
-    p->rk_traces = desc->family == TDG_LGL && d.nmface == 0 && !p->tma;
+    p->rk_traces = desc->family == TDG_LGL && d.nmface == 0;
     int dev = 0, nsm = 0;
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
@@ -891,6 +919,19 @@ int tdg_tau(tdg_plan* p, const double* Q, const double* S, double* tau, int isol
   return dispatch_eval<MODE_TAU>(p, Q, isolated, a, st);
 }
 
+int tdg_tau_from_avalue(tdg_plan* p, const double* A, const double* S, double* tau, void* stream) {
+  if (!p || !A || !tau) return fail(TDG_E_ARG, "null argument");
+  cudaStream_t st = as_stream(stream);
+  if (p->d.nwork == 0) return TDG_OK;
+  KTimer kt(TDG_K_NORM, st);
+  if (p->nv == 5)
+    k_tau_avalue<5><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, A, S, tau);
+  else
+    k_tau_avalue<1><<<p->d.nwork, ELEM_THREADS, 0, st>>>(p->d, A, S, tau);
+  LAUNCH_CHECK("k_tau_avalue");
+  return TDG_OK;
+}
+
 int tdg_rk3_stage(tdg_plan* p, double* Q, double* W, const double* S, int stage, const double* dt,
                   int local, double* rnorm, int32_t* nonfinite, void* stream) {
   return tdg_rk3_stage_ex(p, Q, W, S, stage, dt, local, rnorm, nonfinite, 0, stream);
@@ -970,11 +1011,23 @@ int tdg_check_finite(tdg_plan* p, const double* X, int32_t* flag, void* stream) 
   return TDG_OK;
 }
 
-int tdg_copy_gradient(tdg_plan* p, double* dst, void* stream) {
-  if (!p || !dst) return fail(TDG_E_ARG, "null argument");
+int tdg_gradient(tdg_plan* p, const double* Q, int isolated, double* dst, void* stream) {
+  if (!p || !Q || !dst) return fail(TDG_E_ARG, "null argument");
   if (!p->viscous) return fail(TDG_E_CONFIG, "inviscid plan has no gradient");
-  CUDA_TRY(cudaMemcpyAsync(dst, p->d.grad, sizeof(double) * p->nodes * 3 * p->ngv,
-                           cudaMemcpyDeviceToDevice, as_stream(stream)));
+  // one trace + lift pass that stores the per-node gradient straight into dst
+  DevPlan d = p->d;
+  d.grad = dst;
+  switch (p->d.law) {
+    case TDG_LAW_ADVDIFF: return run_surface<LAW_ADVDIFF>(p, d, Q, isolated, as_stream(stream), false, true);
+    case TDG_LAW_BURGERS: return run_surface<LAW_BURGERS>(p, d, Q, isolated, as_stream(stream), false, true);
+    default: return run_surface<LAW_NS>(p, d, Q, isolated, as_stream(stream), false, true);
+  }
+}
+
+int tdg_plan_info(const tdg_plan* p, int32_t* recompute, int32_t* nwork) {
+  if (!p) return fail(TDG_E_ARG, "null plan");
+  if (recompute) *recompute = p->d.recompute;
+  if (nwork) *nwork = p->d.nwork;
   return TDG_OK;
 }
 

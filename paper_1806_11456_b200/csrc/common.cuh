@@ -16,6 +16,7 @@ constexpr int TABLES_LEN = OFF_T + PAD * PAD * PAD * PAD;
 constexpr int ELEM_THREADS = 256;     // element kernels: 8 warps
 constexpr int MAXN = 512;             // nodes per element work item (<= (7+1)^3)
 constexpr int NPT = MAXN / ELEM_THREADS;
+constexpr int MAX_ITEM_ELEMS = 64;    // elements per work item (per-element smem reductions)
 constexpr int FACE_THREADS = 64;      // one interior face (<= 8x8 mortar nodes) per block
 constexpr int FACE_THREADS_MAX = 128; // packed uniform faces: face_pack * face_nm <= 128
 constexpr int SIDE_THREADS = 256;     // four element sides per block
@@ -53,8 +54,12 @@ struct DevPlan {
   const int* work_ord;   // per work item: its (N1, N2, N3), read without waiting for work[]
   int nsm;        // SMs: kernels prefetch the work about one wave ahead (L2)
   int pf_trace, pf_face, pf_down;   // look-ahead distances, blocks per SM
-  int div_mma;    // weak divergence of the flux kernel on the FP64 tensor cores
-  int pf_item;    // flux kernel: L2 bulk prefetch of the item's Q and grad spans
+  int pf_item;    // element kernels: L2 bulk prefetch of the item's own spans
+  // BR1 gradient recomputed inside the flux kernel (every work item affine):
+  // the lift kernel writes only the gradient's side traces and no per-node
+  // gradient (12 doubles per node written once and read once less)
+  int recompute;
+  int collapsed;  // bit d: direction d has order 0 on every element (2D extrusion)
   // side work items for side kernels: (slot, side | kind<<8), ghost offset
   int nside_iso;
   const int4* side_iso;      // isolated: every side of every element
@@ -83,7 +88,7 @@ struct DevPlan {
   double* lsurf;  // [side_nodes][3*ngv]   lift surface contributions
   double* gtr;    // [side_nodes][3*ngv] own-order gradient traces
   double* fsurf;  // [side_nodes][nv]      flux surface contributions
-  double* grad;   // [nodes][3*ngv]        lifted gradient
+  double* grad;   // [nodes][3*ngv] lifted gradient (NULL: not stored, see recompute)
   // conforming-face lift in g* form (LGL plans without nonconforming faces):
   // k_face<lift> writes g* = ½(g_L + g_R) once per face node ([ngv][nm] at
   // the left side's trace offset) instead of g*·n σ for both sides (2 x 3 ngv),
@@ -210,67 +215,17 @@ __device__ __forceinline__ void l2_prefetch_span(const void* p, size_t bytes) {
                : "memory");
 }
 
+// a[i] for i in 0..2 as selects (a runtime index into a local array would
+// put the array in local memory)
+__device__ __forceinline__ int sel3(int i, int a0, int a1, int a2) {
+  return i == 0 ? a0 : (i == 1 ? a1 : a2);
+}
+
 // face coordinates of a side: normal direction and the two tangential ones
 __device__ __forceinline__ void side_dirs(int side, int& d, int& a, int& b) {
   d = side >> 1;
   a = (d == 0) ? 1 : 0;
   b = (d == 2) ? 1 : 2;
-}
-
-}  // namespace tdg
-
-// ---------------------------------------------------------------------------
-// TMA bulk copies (cp.async.bulk) completing on an mbarrier
-namespace tdg {
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// Copy doubles [src, src+count) into shared memory at a 16-byte aligned
-// ``dst`` with one bulk copy; returns the index offset (0 or 1) at which the
-// data starts in ``dst`` (the source span is widened to 16-byte boundaries,
-// so buffers need >= 8 bytes of slack past their end).
-__device__ __forceinline__ int bulk_span(double* dst, const double* src, long long count,
-                                         unsigned long long* bar, uint32_t& bytes_total) {
-  const unsigned long long a = reinterpret_cast<unsigned long long>(src);
-  const unsigned long long lo = a & ~15ull;
-  const unsigned long long hi = (a + 8ull * count + 15ull) & ~15ull;
-  const uint32_t bytes = static_cast<uint32_t>(hi - lo);
-  bulk_g2s(dst, reinterpret_cast<const void*>(lo), bytes, bar);
-  bytes_total += bytes;
-  return static_cast<int>((a - lo) >> 3);
 }
 
 }  // namespace tdg

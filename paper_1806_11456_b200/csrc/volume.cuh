@@ -17,25 +17,24 @@ struct ElemTables {
   double w[3][8];
   double bnd[3][16];  // l_i(-1) at [i], l_i(+1) at [8+i]
   double red[32];
-  unsigned long long emax[64];  // per-element max bits (tau / dt)
+  unsigned long long emax[MAX_ITEM_ELEMS];  // per-element max bits (tau / dt)
 };
 
 __device__ __forceinline__ void load_tables(const DevPlan& P, int N1, int N2, int N3,
                                             ElemTables& T) {
-  const int No[3] = {N1, N2, N3};
   for (int u = threadIdx.x; u < 3 * 64; u += blockDim.x) {
     const int d = u / 64, k = u % 64;
-    T.dh[d][k] = P.tables[OFF_DHAT + No[d] * 64 + k];
+    T.dh[d][k] = P.tables[OFF_DHAT + sel3(d, N1, N2, N3) * 64 + k];
   }
   for (int u = threadIdx.x; u < 3 * 8; u += blockDim.x) {
     const int d = u / 8, k = u % 8;
-    T.w[d][k] = P.tables[OFF_W + No[d] * 8 + k];
+    T.w[d][k] = P.tables[OFF_W + sel3(d, N1, N2, N3) * 8 + k];
   }
   for (int u = threadIdx.x; u < 3 * 16; u += blockDim.x) {
     const int d = u / 16, k = u % 16;
-    T.bnd[d][k] = P.tables[OFF_BND + No[d] * 16 + k];
+    T.bnd[d][k] = P.tables[OFF_BND + sel3(d, N1, N2, N3) * 16 + k];
   }
-  for (int u = threadIdx.x; u < 64; u += blockDim.x) T.emax[u] = 0ull;
+  for (int u = threadIdx.x; u < MAX_ITEM_ELEMS; u += blockDim.x) T.emax[u] = 0ull;
 }
 
 __device__ __forceinline__ const double* metric_ptr(const DevPlan& P, int slot, int node, int n,
@@ -76,10 +75,13 @@ __device__ __forceinline__ void item_side_traces(const DevPlan& P, int slot0, in
     const int e = task / 6, s = task % 6, slot = slot0 + e;
     int d, a, b;
     side_dirs(s, d, a, b);
-    const int na = np[a], nb = np[b], nf = na * nb, nd = np[d];
-    const int sa = strides[a], sb = strides[b], sd = strides[d];
+    const int na = sel3(a, np[0], np[1], np[2]), nb = sel3(b, np[0], np[1], np[2]);
+    const int nd = sel3(d, np[0], np[1], np[2]), nf = na * nb;
+    const int sa = sel3(a, strides[0], strides[1], strides[2]);
+    const int sb = sel3(b, strides[0], strides[1], strides[2]);
+    const int sd = sel3(d, strides[0], strides[1], strides[2]);
     const int last = (s & 1) ? (nd - 1) * sd : 0;
-    const double* row = &bnd[d][(s & 1) * 8];
+    const double* row = bnd[d] + (s & 1) * 8;
     auto tr = [&](int c, int ia, int ib) -> double {
       const int off0 = ia * sa + ib * sb;
       if (lgl) return vol(e, c, off0 + last);
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
   const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int No[3] = {od[0], od[1], od[2]};
   for (int u = threadIdx.x; u < 48; u += blockDim.x)
-    sb[u / 16][u % 16] = P.tables[OFF_BND + No[u / 16] * 16 + (u % 16)];
+    sb[u / 16][u % 16] = P.tables[OFF_BND + sel3(u / 16, No[0], No[1], No[2]) * 16 + (u % 16)];
   __syncthreads();
   const int np[3] = {No[0] + 1, No[1] + 1, No[2] + 1};
   const int n = np[0] * np[1] * np[2];
@@ -185,19 +187,21 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
     for (int u = threadIdx.x; u < wi.y * per_e; u += blockDim.x) {
       const int e = u / per_e;
       int r = u - e * per_e, s = 0;
-      while (r >= nfs[s >> 1]) {
-        r -= nfs[s >> 1];
+      while (r >= sel3(s >> 1, nfs[0], nfs[1], nfs[2])) {
+        r -= sel3(s >> 1, nfs[0], nfs[1], nfs[2]);
         ++s;
       }
       int d, a, b;
       side_dirs(s, d, a, b);
-      const int na = np[a], nf = nfs[d], nd = np[d];
+      const int na = sel3(a, np[0], np[1], np[2]), nf = sel3(d, nfs[0], nfs[1], nfs[2]);
+      const int nd = sel3(d, np[0], np[1], np[2]);
       const int ib = r / na, ia = r - ib * na;
       const int slot = wi.x + e;
-      const double* q = Q + P.node_off[slot] * NV + ia * strides[a] + ib * strides[b];
+      const double* q = Q + P.node_off[slot] * NV + ia * sel3(a, strides[0], strides[1], strides[2]) +
+                        ib * sel3(b, strides[0], strides[1], strides[2]);
       double* dst = P.qtr + P.side_off[slot * 6 + s] * NV + r;
-      const int sd = strides[d];
-      const double* row = &sb[d][(s & 1) * 8];
+      const int sd = sel3(d, strides[0], strides[1], strides[2]);
+      const double* row = sb[d] + (s & 1) * 8;
 #pragma unroll
       for (int c = 0; c < NV; ++c) {
         double acc;
@@ -476,7 +480,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
 #pragma unroll
       for (int c = 0; c < NG; ++c) {
         G[c * tot + t] = Greg[r][c];
-        P.grad[gb + (long long)c * n + node] = Greg[r][c];
+        if (P.grad) P.grad[gb + (long long)c * n + node] = Greg[r][c];
       }
     }
   }
@@ -490,14 +494,48 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
   }
 }
 
+// Face nodes of an LGL element with (n1p, n2p, n3p) >= 2 points per
+// direction: the planes k = 0 and k = N3 first, then the rings (j = 0,
+// j = N2, i = 0, i = N1) of the inner planes.
+__device__ __forceinline__ int face_node_count(int n1p, int n2p, int n3p) {
+  return 2 * n1p * n2p + (n3p - 2) * (2 * n1p + 2 * (n2p - 2));
+}
+
+__device__ __forceinline__ void face_node(int f, int n1p, int n2p, int n3p, int& i, int& j, int& k) {
+  const int pl = n1p * n2p;
+  if (f < 2 * pl) {
+    k = f < pl ? 0 : n3p - 1;
+    const int g = f < pl ? f : f - pl;
+    j = g / n1p;
+    i = g - j * n1p;
+    return;
+  }
+  const int ring = 2 * n1p + 2 * (n2p - 2);
+  const int g = f - 2 * pl;
+  k = 1 + g / ring;
+  const int p = g - (k - 1) * ring;
+  if (p < 2 * n1p) {
+    j = p < n1p ? 0 : n2p - 1;
+    i = p < n1p ? p : p - n1p;
+  } else {
+    const int q = p - 2 * n1p;
+    j = 1 + (q >> 1);
+    i = (q & 1) ? n1p - 1 : 0;
+  }
+}
+
 // BR1 lift for LGL plans whose evaluated sides all use own-order traces (no
 // nonconforming face, or an isolated evaluation): the side traces of G are
-// face-node values, so every node writes its gradient straight to ``grad``
-// and to the own-order trace arrays of the sides it lies on.  No staging of
-// G in shared memory and no second barrier, so each thread keeps one node's
-// values at a time (80 registers without spills, 3 blocks per SM: measured
-// faster than 4 blocks with spills at 64).
-template <int LAW, int NX>
+// face-node values, so every node writes its gradient straight to the
+// own-order trace arrays of the sides it lies on (and to ``grad`` when the
+// plan stores it).  No staging of G in shared memory and no second barrier,
+// so each thread keeps one node's values at a time (80 registers, 3 blocks
+// per SM: measured faster than 4 blocks with spills at 64).
+//
+// FACE_ONLY (plans whose flux kernel recomputes G, P.recompute): only the
+// face nodes are lifted — the interior gradient is never needed here.  An
+// N=7 element has 296 face nodes of 512.
+template <int LAW, int NX, bool FACE_ONLY>
 __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, const double* __restrict__ Q,
                                                                    int coupled) {
   using L = Law<LAW>;
@@ -523,32 +561,41 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
   // staging needs no table: one barrier covers both
   stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
   __syncthreads();
-  const int np[3] = {n1p, n2p, n3p};
+  const int nfn = FACE_ONLY ? face_node_count(n1p, n2p, n3p) : n;
+  const int tasks = wi.y * nfn;
 #pragma unroll 1
-  for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * blockDim.x;
-    if (t < tot) {
-      const int e = t / n, node = t - e * n, slot = wi.x + e;
-      const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
-      double x[NG];
-      if (coupled && P.gstar)
-        lift_node<LAW, NX, true>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
-      else
-        lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+  for (int t = threadIdx.x; t < tasks; t += blockDim.x) {
+    const int e = t / nfn, f = t - e * nfn, slot = wi.x + e;
+    int i, j, k;
+    if (FACE_ONLY) {
+      face_node(f, n1p, n2p, n3p, i, j, k);
+    } else {
+      i = f % n1p;
+      j = (f / n1p) % n2p;
+      k = f / (n1p * n2p);
+    }
+    const int node = i + n1p * (j + n2p * k);
+    double x[NG];
+    if (coupled && P.gstar)
+      lift_node<LAW, NX, true>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+    else
+      lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+    if (!FACE_ONLY && P.grad) {
       const long long gb = P.node_off[slot] * NG;
 #pragma unroll
       for (int c = 0; c < NG; ++c) P.grad[gb + (long long)c * n + node] = x[c];
-      const int ijk[3] = {i, j, k};
+    }
+    const int ijk[3] = {i, j, k};
+    const int np[3] = {n1p, n2p, n3p};
 #pragma unroll
-      for (int s = 0; s < 6; ++s) {
-        int d, a, b;
-        side_dirs(s, d, a, b);
-        if (ijk[d] != ((s & 1) ? np[d] - 1 : 0)) continue;
-        const int nf = np[a] * np[b];
-        double* dst = P.gtr + P.side_off[slot * 6 + s] * NG + ijk[a] + np[a] * ijk[b];
+    for (int s = 0; s < 6; ++s) {
+      int d, a, b;
+      side_dirs(s, d, a, b);
+      if (ijk[d] != ((s & 1) ? np[d] - 1 : 0)) continue;
+      const int nf = np[a] * np[b];
+      double* dst = P.gtr + P.side_off[slot * 6 + s] * NG + ijk[a] + np[a] * ijk[b];
 #pragma unroll
-        for (int c = 0; c < NG; ++c) dst[(long long)c * nf] = x[c];
-      }
+      for (int c = 0; c < NG; ++c) dst[(long long)c * nf] = x[c];
     }
   }
 }
@@ -569,76 +616,85 @@ struct FluxArgs {
   double* norm;        // max |r|
   int* nonfinite;
   int traces;          // RK: also write the new state's own-order Q traces (LGL, conforming)
+  int coupled;         // coupled (1) or isolated (0) evaluation (the lift's surface terms)
 };
 
-// ---------------------------------------------------------------------------
-// Weak divergence on the FP64 tensor cores (operators.py:196-200): for each
-// direction d and component c, the item's d-lines (all E elements, same
-// orders) are contracted 8 lines at a time with the weighted derivative
-// matrix, D(i, line) = sum_m Dhat_d[m][i] ft_d[c](m, line) (mma.m8n8k4, one
-// or two k-steps), scaled by the line's tangential weights.  The result
-// accumulates in place in direction 0's array ft[0][c] (direction 0 first,
-// then += 1, then += 2: the ((x + y) + z) order of the scalar chains); each
-// tile's outputs are the nodes of its own lines, so the in-place direction-0
-// pass is warp-local.  One block barrier after each direction.  Replaces
-// ~3(N+1) shared-memory loads per node and component by 2 per 8 outputs.
-template <int C>
-__device__ __forceinline__ void item_weak_div_mma(const ElemTables& T, double* ft, int tot, int n,
-                                                  int n1p, int n2p, int n3p) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int g = lane >> 2, q = lane & 3;
-  const int np[3] = {n1p, n2p, n3p};
-  const int st[3] = {1, n1p, n1p * n2p};
-  const int E = tot / n;
-#pragma unroll 1
-  for (int d = 0; d < 3; ++d) {
-    const int a = (d == 0) ? 1 : 0, b = (d == 2) ? 1 : 2;
-    const int nd = np[d], na = np[a], sd = st[d], sa = st[a], sb = st[b];
-    const int lines_e = na * np[b], nlines = E * lines_e, ntiles = (nlines + 7) >> 3;
-    const double a0 = (g < nd && q < nd) ? T.dh[d][q * 8 + g] : 0.0;
-    const double a1 = (g < nd && q + 4 < nd) ? T.dh[d][(q + 4) * 8 + g] : 0.0;
-    const bool k2 = nd > 4;
-    // node base and tangential weight of line L (-1: past the end)
-    auto line = [&](int L, double& w) -> int {
-      if (L >= nlines) return -1;
-      const int e = L / lines_e, r = L - e * lines_e, ib = r / na, ia = r - ib * na;
-      w = T.w[a][ia] * T.w[b][ib];
-      return e * n + ia * sa + ib * sb;
-    };
-#pragma unroll 1
-    for (int tile = warp; tile < ntiles; tile += nw) {
-      // line geometry once per tile; the C components' MMA chains interleave
-      double wl, w0, w1;
-      const int bl = line(tile * 8 + g, wl);
-      const int o0 = line(tile * 8 + 2 * q, w0), o1 = line(tile * 8 + 2 * q + 1, w1);
-      const bool l0 = bl >= 0 && q < nd, l1 = bl >= 0 && k2 && q + 4 < nd;
-      const int i0 = bl + q * sd, i1 = bl + (q + 4) * sd;
-      const bool s0 = g < nd && o0 >= 0, s1 = g < nd && o1 >= 0;
-      const int j0 = o0 + g * sd, j1 = o1 + g * sd;
-      double d0[C], d1[C];
+// Contravariant fluxes f~_i = Ja^i . (f_a - f_v) of an affine work item with
+// the BR1 gradient recomputed in place (P.recompute): g(q) is staged in the
+// direction-2 flux region, each node's G comes from lift_node (the same
+// arithmetic the lift kernel uses), f~_0, f~_1 go to shared memory at once
+// and f~_2 waits in registers until every thread has finished reading g.
+// Shared memory stays [3][NV][tot] (3 blocks per SM), and the 12-double
+// gradient never touches HBM.
+template <int LAW, int NX>
+__device__ __forceinline__ void item_fluxes_recompute(const DevPlan& P, const double* __restrict__ Q,
+                                                      const FluxArgs& A, int2 wi, int N1, int N2, int N3,
+                                                      ElemTables& T, double* ft) {
+  using L = Law<LAW>;
+  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
+  const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
+  const int n = n1p * n2p * n3p, tot = wi.y * n;
+  double qa[NPT][NV];
+  load_item_state<NV>(P, Q, wi, n, tot, qa);
+  load_tables(P, N1, N2, N3, T);
+  double* gs = ft + 2 * NV * tot;   // [NGV][tot] inside the direction-2 region
+  stage_grad_vars<LAW>(P, wi, n, tot, true, qa, gs, nullptr);
+  __syncthreads();
+  const bool gstar = A.coupled && P.gstar;
+  double f2[NPT][NV];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const double* src = ft + (d * C + c) * tot;
-        const double b0 = l0 ? src[i0] : 0.0;
-        const double b1 = l1 ? src[i1] : 0.0;
-        d0[c] = 0.0;
-        d1[c] = 0.0;
-        dmma_8x8x4(d0[c], d1[c], a0, b0);
-        if (k2) dmma_8x8x4(d0[c], d1[c], a1, b1);
-      }
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * blockDim.x;
+    if (t < tot) {
+      const int e = t / n, node = t - e * n, slot = wi.x + e;
+      const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+      double G[NG];
+      if (gstar)
+        lift_node<LAW, NX, true>(P, T, gs, nullptr, true, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, G);
+      else
+        lift_node<LAW, NX>(P, T, gs, nullptr, true, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, G);
+      double f[3][NV], Gd[3][NGV];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        double* acc = ft + c * tot;
-        if (s0) acc[j0] = d == 0 ? d0[c] * w0 : acc[j0] + d0[c] * w0;
-        if (s1) acc[j1] = d == 0 ? d1[c] * w1 : acc[j1] + d1[c] * w1;
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) Gd[d][kk] = G[d * NGV + kk];
+      L::adv_flux(P.prm, qa[r], f);
+      L::sub_visc(P.prm, qa[r], Gd, f);
+      const double* m = P.metrics + P.metric_off[slot];
+#pragma unroll
+      for (int ii = 0; ii < 3; ++ii) {
+        const double j0 = m[1 + 3 * ii], j1 = m[2 + 3 * ii], j2 = m[3 + 3 * ii];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double x = j0 * f[0][v] + j1 * f[1][v] + j2 * f[2][v];
+          if (ii < 2)
+            ft[(ii * NV + v) * tot + t] = x;
+          else
+            f2[r][v] = x;
+        }
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * blockDim.x;
+    if (t < tot) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) ft[(2 * NV + v) * tot + t] = f2[r][v];
+    }
+  }
+  __syncthreads();
 }
 
-template <int LAW, int MODE, int NX>
-__global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
+// REC: the plan recomputes the gradient (every item affine, viscous law);
+// its lift + flux working set needs more than 80 registers, so REC blocks
+// run REC_BLOCKS per SM.
+#ifndef REC_BLOCKS
+#define REC_BLOCKS 2
+#endif
+template <int LAW, int MODE, int NX, bool REC>
+__global__ void __launch_bounds__(ELEM_THREADS, REC ? REC_BLOCKS : 3) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
@@ -650,7 +706,14 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   // epilogue inputs, read after the contraction
   if (MODE != MODE_F) prefetch_item_nodes<NV>(P, MODE == MODE_A ? A.X : A.S, wi, 32);
   if (MODE == MODE_RK && A.stage != 0) prefetch_item_nodes<NV>(P, A.W, wi, 64);
-  if (P.pf_item) {
+  if (REC) {
+    // the lift's surface terms, read by the recomputed gradient
+    if (A.coupled && P.gstar) {
+      if (threadIdx.x >= 96) prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
+    } else {
+      if (threadIdx.x == 96) prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+    }
+  } else if (P.pf_item) {
     // the item's state and gradient spans, read node by node below (the
     // second node of each thread only after the first one's flux)
     prefetch_item_nodes<NV>(P, Q, wi, 96);
@@ -659,46 +722,47 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   }
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
-  const bool visc = L::viscous(P.prm);
   double* ft = sm;   // [3][NV][tot]
-  // the contravariant fluxes need no table: they are formed first, the
-  // tables are staged after them, and one barrier covers both
-
+  if (REC) {
+    item_fluxes_recompute<LAW, NX>(P, Q, A, wi, N1, N2, N3, T, ft);
+  } else {
+    const bool visc = L::viscous(P.prm);
+    // the contravariant fluxes need no table: they are formed first, the
+    // tables are staged after them, and one barrier covers both
 #pragma unroll 1
-  for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * blockDim.x;
-    if (t < tot) {
-      const int e = t / n, node = t - e * n, slot = wi.x + e;
-      const long long base = P.node_off[slot] * NV;
-      double q[NV], f[3][NV];
+    for (int r = 0; r < NPT; ++r) {
+      const int t = threadIdx.x + r * blockDim.x;
+      if (t < tot) {
+        const int e = t / n, node = t - e * n, slot = wi.x + e;
+        const long long base = P.node_off[slot] * NV;
+        double q[NV], f[3][NV];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) q[v] = Q[base + (long long)v * n + node];
-      L::adv_flux(P.prm, q, f);
-      if (visc) {
-        double G[3][NGV];
-        const double* gp = P.grad + P.node_off[slot] * NG + node;
+        for (int v = 0; v < NV; ++v) q[v] = Q[base + (long long)v * n + node];
+        L::adv_flux(P.prm, q, f);
+        if (visc) {
+          double G[3][NGV];
+          const double* gp = P.grad + P.node_off[slot] * NG + node;
 #pragma unroll
-        for (int d = 0; d < 3; ++d)
+          for (int d = 0; d < 3; ++d)
 #pragma unroll
-          for (int k = 0; k < NGV; ++k) G[d][k] = gp[(long long)(d * NGV + k) * n];
-        L::sub_visc(P.prm, q, G, f);
-      }
-      int ms;
-      const double* m = metric_ptr(P, slot, node, n, ms);
+            for (int k = 0; k < NGV; ++k) G[d][k] = gp[(long long)(d * NGV + k) * n];
+          L::sub_visc(P.prm, q, G, f);
+        }
+        int ms;
+        const double* m = metric_ptr(P, slot, node, n, ms);
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const double j0 = m[(1 + 3 * i) * ms], j1 = m[(2 + 3 * i) * ms], j2 = m[(3 + 3 * i) * ms];
+        for (int i = 0; i < 3; ++i) {
+          const double j0 = m[(1 + 3 * i) * ms], j1 = m[(2 + 3 * i) * ms], j2 = m[(3 + 3 * i) * ms];
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
-          ft[(i * NV + v) * tot + t] = j0 * f[0][v] + j1 * f[1][v] + j2 * f[2][v];
+          for (int v = 0; v < NV; ++v)
+            ft[(i * NV + v) * tot + t] = j0 * f[0][v] + j1 * f[1][v] + j2 * f[2][v];
+        }
       }
     }
+    load_tables(P, N1, N2, N3, T);
+    __syncthreads();
   }
-  load_tables(P, N1, N2, N3, T);
-  __syncthreads();
 
-  const bool mma_div = P.div_mma != 0;
-  if (mma_div) item_weak_div_mma<NV>(T, ft, tot, n, n1p, n2p, n3p);
   double rmax = 0.0;
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
@@ -713,10 +777,6 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
         F[v] = 0.0;
         F0[v] = F1[v] = F2[v] = 0.0;
       }
-      if (mma_div) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) F0[v] = ft[v * tot + t];
-      } else {
       {
         const double wo = T.w[1][j] * T.w[2][k];
 #pragma unroll
@@ -749,7 +809,6 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
 #pragma unroll
           for (int v = 0; v < NV; ++v) F2[v] += dw * ft[(2 * NV + v) * tot + idx];
         }
-      }
       }
 #pragma unroll
       for (int v = 0; v < NV; ++v) F[v] -= (F0[v] + F1[v]) + F2[v];
@@ -792,7 +851,10 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
           rmax = nanmax(rmax, fabs(rv));
         }
       } else if (MODE == MODE_RK) {
-        const double dtv = A.local ? A.dt[slot] : A.dt[0];
+        const double dtv0 = A.local ? A.dt[slot] : A.dt[0];
+        // no time scale (dt = +inf): leave Q untouched; the caller raises
+        // TimeScaleError as the reference does before stepping (timestep.py:133)
+        const double dtv = isinf(dtv0) && dtv0 > 0.0 ? 0.0 : dtv0;
         bool bad = false;
         double qn[NV];
 #pragma unroll
@@ -812,7 +874,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
           // LGL face nodes: the next stage's own-order Q traces (k_trace_q skipped)
           const int ijk[3] = {i, j, k};
           const int np[3] = {n1p, n2p, n3p};
-#pragma unroll 1
+#pragma unroll
           for (int sd = 0; sd < 6; ++sd) {
             int d, a, b;
             side_dirs(sd, d, a, b);
@@ -852,12 +914,12 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_element_dt(DevPlan P, const do
                                                              double* dt_slot, double* dt_min) {
   using L = Law<LAW>;
   constexpr int NV = L::NV;
-  __shared__ unsigned long long smax[64];
+  __shared__ unsigned long long smax[MAX_ITEM_ELEMS];
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int No[3] = {od[0], od[1], od[2]};
   const int n = (No[0] + 1) * (No[1] + 1) * (No[2] + 1), tot = wi.y * n;
-  for (int u = threadIdx.x; u < 64; u += blockDim.x) smax[u] = 0ull;
+  for (int u = threadIdx.x; u < MAX_ITEM_ELEMS; u += blockDim.x) smax[u] = 0ull;
   __syncthreads();
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
     const int e = t / n, node = t - e * n, slot = wi.x + e;
@@ -874,8 +936,11 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_element_dt(DevPlan P, const do
     const int slot = wi.x + e;
     const double sm = __longlong_as_double((long long)smax[e]);
     double dt = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
     for (int d = 0; d < 3; ++d) {
-      if (No[d] == 0) continue;
+      // collapsed directions (order 0 on every element) carry no time scale;
+      // any other direction uses max(N_d, 1) (timestep.py:55)
+      if ((P.collapsed >> d) & 1) continue;
       const double nn = (double)(No[d] > 1 ? No[d] : 1);
       const double h = P.sizes[slot * 3 + d];
       if (sm > 0.0) dt = fmin(dt, cfl_a * h / (sm * nn * nn));
@@ -892,12 +957,12 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_element_dt(DevPlan P, const do
 template <int NV>
 __global__ void __launch_bounds__(ELEM_THREADS) k_norm(DevPlan P, const double* __restrict__ X,
                                                        double* gmax, double* emax_out, int* flag) {
-  __shared__ unsigned long long emax[64];
+  __shared__ unsigned long long emax[MAX_ITEM_ELEMS];
   __shared__ double red[32];
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int n = (od[0] + 1) * (od[1] + 1) * (od[2] + 1), tot = wi.y * n;
-  for (int u = threadIdx.x; u < 64; u += blockDim.x) emax[u] = 0ull;
+  for (int u = threadIdx.x; u < MAX_ITEM_ELEMS; u += blockDim.x) emax[u] = 0ull;
   __syncthreads();
   double m = 0.0;
   bool bad = false;
@@ -921,6 +986,42 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_norm(DevPlan P, const double* 
     for (int e = threadIdx.x; e < wi.y; e += blockDim.x)
       emax_out[P.elem_id[wi.x + e]] = __longlong_as_double((long long)emax[e]);
   }
+}
+
+// ---------------------------------------------------------------------------
+// truncation_from_avalue (operators.py:355-360): tau[elem] = max over nodes and
+// unknowns of |M (S - A)|, M = w_i w_j w_k J as in the MODE_TAU epilogue.
+template <int NV>
+__global__ void __launch_bounds__(ELEM_THREADS) k_tau_avalue(DevPlan P, const double* __restrict__ A,
+                                                             const double* __restrict__ S, double* tau) {
+  __shared__ unsigned long long emax[MAX_ITEM_ELEMS];
+  __shared__ double w[3][8];
+  const int2 wi = P.work[blockIdx.x];
+  const int* od = P.work_ord + 3 * blockIdx.x;
+  const int n1p = od[0] + 1, n2p = od[1] + 1, n = n1p * n2p * (od[2] + 1), tot = wi.y * n;
+  for (int u = threadIdx.x; u < MAX_ITEM_ELEMS; u += blockDim.x) emax[u] = 0ull;
+  for (int u = threadIdx.x; u < 24; u += blockDim.x)
+    w[u / 8][u % 8] = P.tables[OFF_W + sel3(u / 8, od[0], od[1], od[2]) * 8 + (u % 8)];
+  __syncthreads();
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int e = t / n, node = t - e * n, slot = wi.x + e;
+    const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+    int ms;
+    const double* mp = metric_ptr(P, slot, node, n, ms);
+    const double mass = w[0][i] * w[1][j] * w[2][k] * mp[0];
+    const long long base = P.node_off[slot] * NV + node;
+    double tv = 0.0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const long long ix = base + (long long)v * n;
+      const double s = S ? S[ix] : 0.0;
+      tv = nanmax(tv, fabs(mass * (s - A[ix])));
+    }
+    atomicMax(&emax[e], static_cast<unsigned long long>(__double_as_longlong(tv)));
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < wi.y; e += blockDim.x)
+    tau[P.elem_id[wi.x + e]] = __longlong_as_double((long long)emax[e]);
 }
 
 }  // namespace tdg

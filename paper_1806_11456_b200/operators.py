@@ -156,20 +156,15 @@ class DGOperator:
         self._params = params
         self._tables = spectral.device_tables(fam)
         self._create_plan()
-        # mass per node and per unknown (host) for truncation_from_avalue / mass_blocks
+        # mass per node (host) for mass_blocks
         mass = np.zeros(of.num_nodes)
-        mass_full = np.zeros(of.num_nodes * self.nv)
         for g, (sig, ids) in enumerate(zip(of.group_orders, of.group_elements)):
             w = [spectral.rule(n, fam)[1] for n in sig]
             www = w[0][:, None, None] * w[1][None, :, None] * w[2][None, None, :]
             mg = _vol_layout(www[None] * self._jac[g])                 # (B, n)
             s0 = of.group_slot0[g]
             mass[of.node_off[s0]: of.node_off[s0 + len(ids)]] = mg.ravel()
-            a = int(of.node_off[s0]) * self.nv
-            mf = np.repeat(mg[:, None, :], self.nv, axis=1)
-            mass_full[a: a + mf.size] = mf.ravel()
         self._mass_nodes = mass
-        self._mass_full = mass_full
         self._mass_dev = None
 
     def _tan(self, e, side):
@@ -227,9 +222,6 @@ class DGOperator:
         side_info = np.zeros((ns, 6, 4), np.int32)
         side_info[:, :, 2] = -1
         mcap = np.zeros((ns, 6), np.int64)
-        face_m_off = np.full(len(idx_int), -1, np.int64)
-        down = []
-        moff = 0
         if len(info):
             conf = ((info[:, 5] == info[:, 9]) & (info[:, 6] == info[:, 10])
                     & (info[:, 7] == info[:, 9]) & (info[:, 8] == info[:, 10]))
@@ -241,23 +233,12 @@ class DGOperator:
                 side_info[sl, sd, 1] = packed_m
                 side_info[sl, sd, 2] = np.arange(len(info))
                 mcap[sl, sd] = np.where(conf, 0, nm)
-            nc = np.flatnonzero(~conf)
-            face_m_off[nc] = np.concatenate([[0], np.cumsum(nm[nc])])[:-1]
-            moff = int(nm[nc].sum())
-            down = np.stack([np.repeat(nc, 2), np.tile([0, 1], len(nc))], axis=1)
         moffs = np.concatenate([[0], np.cumsum(mcap.ravel())])[:-1].reshape(ns, 6)
         if moffs.size and moffs.max() >= 2 ** 31:
             raise ConfigError("mortar trace offsets exceed 32 bits")
         side_info[:, :, 3] = np.where(mcap > 0, moffs, -1)
-        up = np.argwhere(mcap > 0)
         self._side_info = _as(side_info.ravel(), np.int32)
         self._mtr_nodes = int(mcap.sum())
-        self._up = _as(up.ravel() if len(up) else np.zeros(2, np.int32), np.int32)
-        self._nup = len(up)
-        self._face_m_off = _as(face_m_off if len(face_m_off) else np.zeros(1, np.int64), np.int64)
-        self._mortar_nodes = moff
-        self._down = _as(np.asarray(down).ravel() if len(down) else np.zeros(2, np.int32), np.int32)
-        self._ndown = len(down)
         self._face_info = _as(info.ravel() if len(info) else np.zeros(12, np.int32), np.int32)
         self._nfaces = len(idx_int)
         self._face_geo_off = _as(geo_off if len(geo_off) else np.zeros(1, np.int64), np.int64)
@@ -344,12 +325,6 @@ class DGOperator:
         d.face_geo, d.face_geo_len = _p(self._face_geo, C.c_double), len(self._face_geo)
         d.side_info = _p(self._side_info, C.c_int32)
         d.mtr_nodes = self._mtr_nodes
-        d.nup = self._nup
-        d.up = _p(self._up, C.c_int32)
-        d.face_m_off = _p(self._face_m_off, C.c_int64)
-        d.mortar_nodes = self._mortar_nodes
-        d.ndown = self._ndown
-        d.down = _p(self._down, C.c_int32)
         d.nbfaces = self._nbfaces
         d.bface_info = _p(self._bface_info, C.c_int32)
         d.ghost_off = _p(self._ghost_off, C.c_int64)
@@ -498,19 +473,30 @@ class DGOperator:
 
     def truncation_from_avalue(self, a_value: NodalField):
         """max |M (S_pde - A)| per element (operators.py:355-360), numpy (nel,)."""
+        return self.truncation_from_avalue_device(a_value).cpu().numpy()
+
+    def truncation_from_avalue_device(self, a_value: NodalField, out=None):
+        """The same on the device (tdg_tau_from_avalue): (nel,) by element id."""
         import torch
 
-        if self._mass_dev is None:
-            self._mass_dev = torch.as_tensor(self._mass_full, device=self.device)
-        tmp = NodalField(self.orders, (self.source.data - a_value.data) * self._mass_dev, self.nv)
-        return self.element_norms(tmp).cpu().numpy()
+        self._check_field(a_value)
+        out = out if out is not None else torch.empty(self.orders.num_elements, dtype=torch.float64,
+                                                      device=self.device)
+        _lib.call("tdg_tau_from_avalue", self._plan, _lib.ptr(a_value.data), self._src_ptr(self.source),
+                  _lib.ptr(out), self._stream())
+        return out
 
     def _mass_dev_tensor(self):
-        """Mass per unknown (device), laid out like a NodalField."""
+        """Mass per unknown (device), laid out like a NodalField (tests)."""
         import torch
 
         if self._mass_dev is None:
-            self._mass_dev = torch.as_tensor(self._mass_full, device=self.device)
+            of = self.orders
+            full = np.zeros(of.num_nodes * self.nv)
+            for s0 in range(of.num_elements):
+                a, b = int(of.node_off[s0]), int(of.node_off[s0 + 1])
+                full[a * self.nv: b * self.nv] = np.tile(self._mass_nodes[a:b], self.nv)
+            self._mass_dev = torch.as_tensor(full, device=self.device)
         return self._mass_dev
 
     def norm_inf_device(self, X: NodalField, out=None):
@@ -535,10 +521,19 @@ class DGOperator:
         ([3][ngv][n] per element) — for kernel-level parity tests."""
         import torch
 
-        self.apply(Q, isolated)
+        self._check_field(Q)
         out = torch.empty(self.orders.num_nodes * 3 * self.ngv, dtype=torch.float64, device=self.device)
-        _lib.call("tdg_copy_gradient", self._plan, _lib.ptr(out), self._stream())
+        _lib.call("tdg_gradient", self._plan, _lib.ptr(Q.data), int(bool(isolated)), _lib.ptr(out),
+                  self._stream())
         return out
+
+    @property
+    def recomputes_gradient(self) -> bool:
+        """True when the flux kernel recomputes the BR1 gradient (no per-node
+        gradient in HBM; every work item affine)."""
+        rec = C.c_int32()
+        _lib.call("tdg_plan_info", self._plan, C.byref(rec), None)
+        return bool(rec.value)
 
     def debug_buffer(self, which: int):
         """Face scratch buffer of the last evaluation, as a dict
