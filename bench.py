@@ -32,6 +32,9 @@ sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+# the unmodified reference (pure Python, not present on the GPU box) timed in the
+# build container on its own 2D-scalar analogues of configs 1-2
+REF2D = os.path.join(ROOT, "profiles", "reference_cpu_2d.json")
 METRIC = "NS residual DOF-evals/s; p-multigrid V-cycle ms; % of HBM roofline (1 B200)"
 
 
@@ -187,11 +190,57 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(),
+            "threads_env": {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
+                                                           "MKL_NUM_THREADS")}}
+
+
+def curved_fraction(op):
+    of = op.orders
+    cn = sum(int(of.slot_nodes[s]) for s in range(of.num_elements) if not op._affine_slots[s])
+    return cn / max(1, of.num_nodes)
+
+
+def vcycle_bytes(solver, m_of):
+    """Algorithmic HBM bytes of one pinned-sweep V-cycle: per
+    level 6s fused RK stages (8(60+2m) B/node, + 40 for the FAS source on
+    coarse levels), the other evaluations (finest 2, intermediate 3,
+    coarsest 3c+2 in all; 8(45+2m) B/node), one element_dt read (40 B/node)
+    per sweep and 160 (n_f + n_c) per level pair for the two restrictions and
+    the prolong-add.  m_of(level) = metric doubles per node."""
+    sm = solver.smoother
+    nl = len(solver.levels)
+    vbytes = 0.0
+    for li, lev in enumerate(solver.levels):
+        n = lev.orders.num_nodes
+        m = m_of(lev)
+        src = 0 if li == nl - 1 else 40
+        if li == 0:
+            stages, evals, sweeps = 3 * sm.coarsest_sweeps, 2, sm.coarsest_sweeps
+        else:
+            sweeps = sm.pre_sweeps + sm.post_sweeps
+            stages, evals = 3 * sweeps, (2 if li == nl - 1 else 3)
+        vbytes += n * (stages * (8 * (60 + 2 * m) + src) + evals * (8 * (45 + 2 * m) + src) + sweeps * 40)
+        if li > 0:
+            vbytes += 160 * (n + solver.levels[li - 1].orders.num_nodes)
+    return vbytes
+
+
 def run_b200(args):
     import numpy as np
     import torch
 
-    from paper_1806_11456_b200 import _lib, configs, multigrid, operators
+    from paper_1806_11456_b200 import _lib, configs, multigrid, operators, tau, timestep
 
     ws, rank, local = _dist()
     if not torch.cuda.is_available():
@@ -210,7 +259,23 @@ def run_b200(args):
     def max_over_ranks(x):
         return globals()["max_over_ranks"](x, dist, "cuda")
 
-    # ---- residual throughput, config 3 -------------------------------------
+    stream = torch.cuda.current_stream()
+    peak, peak_kind = _peak_hbm()
+
+    def timed(fn, reps):
+        """Device time (ms) of ``reps`` calls of fn on the current stream, max over ranks."""
+        barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(a.elapsed_time(b))
+
+    # ---- residual throughput, config 3 (headline) -------------------------------
     t_setup = time.perf_counter()
     w = configs.config3()
     op = operators.DGOperator(w.mesh, w.law, w.orders, family=w.family, form=w.form)
@@ -219,40 +284,33 @@ def run_b200(args):
     norm = torch.zeros(1, dtype=torch.float64, device="cuda")
     nodes = w.orders.num_nodes
     setup_s = time.perf_counter() - t_setup
-    stream = torch.cuda.current_stream()
+    m3 = 10.0 * curved_fraction(op)
+
+    def resid():
+        op.residual_device(Q, None, out=R, norm=norm)
+
     for _ in range(args.warmup):
-        op.residual_device(Q, None, out=R, norm=norm)
+        resid()
     torch.cuda.synchronize()
+    # timed region: no per-launch instrumentation; clocks sampled meanwhile
     clocks = Clocks(local)
-    _lib.timing_read()
-    _lib.timing_enable(True)
-    barrier()
-    torch.cuda.synchronize()
     clocks.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        op.residual_device(Q, None, out=R, norm=norm)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
+    ms = timed(resid, args.steps)
     clk = clocks.stop()
-    _lib.timing_enable(False)
-    kt = _lib.timing_read()
-    ms_local = ev0.elapsed_time(ev1)
-    ms = max_over_ranks(ms_local)
     ms_step = ms / args.steps
     value = nodes * args.steps * ws / (ms / 1000.0)
-    launches = int(sum(c for _, c in kt.values()))
 
-    # roofline of the dominant kernel (algorithmic bytes)
-    peak, peak_kind = _peak_hbm()
-    curved_nodes = int(sum(int(op.orders.slot_nodes[s]) for s in range(op.orders.num_elements)
-                           if not op._affine_slots[s]))
-    m_per_node = 10.0 * curved_nodes / nodes
+    # kernel split: the same K evaluations again with the library's per-launch
+    # CUDA events (on the launch stream), for the roofline of the dominant kernel
+    _lib.timing_read()
+    _lib.timing_enable(True)
+    ms_instr = timed(resid, args.steps)
+    _lib.timing_enable(False)
+    kt = _lib.timing_read()
+    launches = int(sum(c for _, c in kt.values()))
     per_node = {
-        "vol_flux": 8.0 * (5 + 12 + 5 + m_per_node),      # Q, grad, metrics -> R
-        "vol_lift": 8.0 * (5 + 12 + m_per_node),          # Q, metrics -> grad
+        "vol_flux": 8.0 * (5 + 12 + 5 + m3),      # Q, grad, metrics -> R
+        "vol_lift": 8.0 * (5 + 12 + m3),          # Q, metrics -> grad
     }
     shares = {k: v[0] for k, v in kt.items() if v[1]}
     dom = max(("vol_flux", "vol_lift"), key=lambda k: shares.get(k, 0.0))
@@ -264,12 +322,43 @@ def run_b200(args):
             traffic = json.load(fh).get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
-    resid_bytes = 8.0 * (45 + 2 * m_per_node) * nodes                    # SURVEY §8d, per evaluation
+    resid_bytes = 8.0 * (45 + 2 * m3) * nodes                    # SURVEY §8d, per evaluation
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                "bytes_per_node": per_node[dom],
+                "bytes_per_node": per_node[dom], "kernel_ms": dom_ms,
                 "residual_eval_frac": resid_bytes / (ms_step / 1000.0) / 1e9 / peak,
+                "residual_bytes_per_node": 8.0 * (45 + 2 * m3),
+                "instrumented_ms_per_step": ms_instr / args.steps,
                 "kernel_ms_per_step": {k: round(v / args.steps, 4) for k, v in shares.items()}}
+
+    # ---- config 3: fused RK3 stages (100 in the protocol) ------------------------
+    rk = None
+    if not args.quick:
+        s = timestep._scratch(op)
+        cfg = timestep.TimeConfig()
+        dt_dev = timestep._device_dt(op, Q, cfg, s)
+        Qw = Q.copy()
+        work = op.new_field()
+        rn = torch.zeros(1, dtype=torch.float64, device="cuda")
+        flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+        state = {"k": 0}
+
+        def stage():
+            k = state["k"] % 3
+            op.rk3_stage(Qw, work, op.source, k, dt_dev, False, rnorm=rn, nonfinite=flag, fresh=k > 0)
+            state["k"] += 1
+
+        for _ in range(3):
+            stage()
+        nst = 3 * max(1, args.steps)
+        ms_rk = timed(stage, nst) / nst
+        rk_bpn = 8.0 * (60 + 2 * m3)
+        rk = {"stages": nst, "ms_per_stage": ms_rk, "dof_evals_per_s": nodes / (ms_rk / 1000.0),
+              "ms_per_100_stages": 100 * ms_rk,
+              "roofline": {"bound": "hbm", "bytes_per_node": rk_bpn, "peak": peak, "unit": "GB/s",
+                           "achieved": rk_bpn * nodes / (ms_rk / 1000.0) / 1e9,
+                           "frac": rk_bpn * nodes / (ms_rk / 1000.0) / 1e9 / peak}}
+        del Qw, work
 
     # ---- end to end through the public API with host buffers -------------------
     # Page-locked host states (4 distinct buffers, cycled) evaluated by the
@@ -286,19 +375,35 @@ def run_b200(args):
     Rh = [outs[k % nbuf] for k in range(args.steps)]
     op.residual_host(Qh[:nbuf], out=Rh[:nbuf])     # untimed: every staging buffer once
     torch.cuda.synchronize()
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    _, host_norms = op.residual_host(Qh, out=Rh)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e_ms = timed(lambda: op.residual_host(Qh, out=Rh), 1)
     e2e = {"value": nodes * args.steps * ws / (e_ms / 1000.0), "unit": "DOF-evals/s",
            "h2d_bytes_per_step": q0.numel() * 8, "d2h_bytes_per_step": q0.numel() * 8 + 8,
            "ms_per_step": e_ms / args.steps, "api": "DGOperator.residual_host (tdg_residual_host)",
            "overlap": "double-buffered: H2D of step k+1 and D2H of step k-1 overlap step k"}
-    del op, Q, R, Qh, Rh, bufs, outs
+    del Qh, Rh, bufs, outs
+
+    # ---- config 3: the tau estimation (isolated, all directions) -----------------
+    tau_est = None
+    if not args.quick:
+        solvers = {}
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tm = tau.estimate(w.mesh, w.law, Q, 1e6, isolated=True, fine_op=op, solvers=solvers)
+        torch.cuda.synchronize()
+        first = time.perf_counter() - t0
+        reps = 3
+        t0 = time.perf_counter()
+        ms_tau = timed(lambda: tau.estimate(w.mesh, w.law, Q, 1e6, isolated=True, fine_op=op, solvers=solvers),
+                       reps) / reps
+        wall_tau = (time.perf_counter() - t0) / reps
+        tau_est = {"ms": ms_tau, "wall_ms": 1e3 * wall_tau, "first_call_with_setup_s": round(first, 1),
+                   "levels_per_direction": {d: len(sv.levels) for d, sv in solvers.items()},
+                   "entries": int(sum(len(tm.tau[e][d]) for e in range(w.mesh.num_elements) for d in range(3))),
+                   "note": "device-event time of a cached-solver estimate (residual + per-direction descent "
+                           "+ isolated evaluations + per-element reductions); first call includes the host "
+                           "construction of the 18 per-direction level operators"}
+        del solvers, tm
+    del op, Q, R
 
     # ---- V-cycle, config 4 --------------------------------------------------------
     vcycle = None
@@ -318,50 +423,59 @@ def run_b200(args):
             solver.v_cycle()
             torch.cuda.synchronize()
             for _ in range(args.vcycles):
-                barrier()
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                solver.v_cycle()
-                b.record(stream)
-                torch.cuda.synchronize()
-                times.append(max_over_ranks(a.elapsed_time(b)))
+                times.append(timed(solver.v_cycle, 1))
         hist = [r["rnorm"] for r in solver.log if r["phase"] in ("post", "coarse") and r["level"] == len(solver.levels)]
-        # algorithmic HBM bytes of one pinned-sweep V-cycle (affine:
-        # m = 0): per level 6s fused RK stages (finest 480 B/node, coarse levels
-        # + 40 for the FAS source) and the other operator evaluations (finest 2,
-        # intermediate 3, coarsest 3c + 2 in all), one element_dt read (40
-        # B/node) per sweep, 160 (n_f + n_c) per level pair for the two
-        # restrictions and the prolong-add
-        sm = w4.smoother
-        nl = len(solver.levels)
-        vbytes = 0.0
-        for li, lev in enumerate(solver.levels):
-            n = lev.orders.num_nodes
-            src = 0 if li == nl - 1 else 40
-            if li == 0:
-                stages, evals, sweeps = 3 * sm["coarsest_sweeps"], 2, sm["coarsest_sweeps"]
-            else:
-                sweeps = sm["pre_sweeps"] + sm["post_sweeps"]
-                stages, evals = 3 * sweeps, (2 if li == nl - 1 else 3)
-            vbytes += n * (stages * (480 + src) + evals * (360 + src) + sweeps * 40)
-            if li > 0:
-                vbytes += 160 * (n + solver.levels[li - 1].orders.num_nodes)
-        vpeak, _ = _peak_hbm()
-        v_roof_ms = vbytes / (vpeak * 1e6)
+        vbytes = vcycle_bytes(solver, lambda lev: 0.0)
+        v_roof_ms = vbytes / (peak * 1e6)
         vcycle = {"config": w4.name, "levels": len(solver.levels), "ms_median": statistics.median(times),
                   "ms_all": [round(t, 3) for t in times], "fine_nodes": w4.orders.num_nodes,
                   "smoother": w4.smoother, "setup_s": round(setup4, 1),
                   "rnorm_post": [float(x) for x in hist[-len(times):]],
-                  "roofline": {"bound": "hbm", "algorithmic_gb": vbytes / 1e9, "peak": vpeak, "unit": "GB/s",
+                  "roofline": {"bound": "hbm", "algorithmic_gb": vbytes / 1e9, "peak": peak, "unit": "GB/s",
                                "roofline_ms": v_roof_ms, "frac": v_roof_ms / statistics.median(times)}}
         del solver
 
-    # small configs: V-cycle latency (CUDA-graph replay of pinned-sweep cycles)
-    small = {}
-    if not args.no_vcycle:
+    # ---- config 5: curved shell residual and V-cycle -------------------------------
+    cfg5 = None
+    if not args.no_vcycle and not args.quick:
         import warnings
 
-        from paper_1806_11456_b200 import timestep
+        w5 = configs.config5()
+        t5 = time.perf_counter()
+        sv = multigrid.FASSolver(w5.mesh, w5.law, w5.orders, smoother=multigrid.SmootherConfig(**w5.smoother),
+                                 time_config=timestep.TimeConfig(**w5.time), family=w5.family, form=w5.form)
+        sv.set_state(sv.finest.op.project_function(w5.init))
+        setup5 = time.perf_counter() - t5
+        op5 = sv.finest.op
+        m5 = 10.0 * curved_fraction(op5)
+        R5 = op5.new_field()
+        n5 = w5.orders.num_nodes
+        for _ in range(3):
+            op5.residual_device(sv.Q, None, out=R5, norm=norm)
+        ms5 = timed(lambda: op5.residual_device(sv.Q, None, out=R5, norm=norm), args.steps) / args.steps
+        bpn5 = 8.0 * (45 + 2 * m5)
+        times = []
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", RuntimeWarning)
+            sv.v_cycle()
+            torch.cuda.synchronize()
+            for _ in range(args.vcycles):
+                times.append(timed(sv.v_cycle, 1))
+        vb5 = vcycle_bytes(sv, lambda lev: 10.0 * curved_fraction(lev.op))
+        cfg5 = {"config": w5.name, "nodes": n5, "setup_s": round(setup5, 1),
+                "residual": {"ms": ms5, "dof_evals_per_s": n5 / (ms5 / 1000.0),
+                             "roofline": {"bound": "hbm", "bytes_per_node": bpn5, "peak": peak, "unit": "GB/s",
+                                          "frac": bpn5 * n5 / (ms5 / 1000.0) / 1e9 / peak}},
+                "vcycle": {"levels": len(sv.levels), "ms_median": statistics.median(times),
+                           "ms_all": [round(t, 3) for t in times], "smoother": w5.smoother, "time": w5.time,
+                           "roofline": {"bound": "hbm", "algorithmic_gb": vb5 / 1e9, "peak": peak,
+                                        "roofline_ms": vb5 / (peak * 1e6),
+                                        "frac": vb5 / (peak * 1e6) / statistics.median(times)}}}
+        del sv, op5, R5
+
+    # small configs: V-cycle latency (CUDA-graph replay of pinned-sweep cycles)
+    if not args.no_vcycle and vcycle is not None:
+        import warnings
 
         for cid in (1, 2):
             wk = configs.CONFIGS[cid]()
@@ -372,22 +486,38 @@ def run_b200(args):
                 warnings.simplefilter("ignore", RuntimeWarning)
                 sv.v_cycle()
                 torch.cuda.synchronize()
-                a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                for _ in range(5):
-                    sv.v_cycle()
-                b2.record(stream)
-                torch.cuda.synchronize()
-            small[f"cfg{cid}_vcycle_ms"] = max_over_ranks(a.elapsed_time(b2) / 5)
+                vcycle[f"cfg{cid}_vcycle_ms"] = timed(sv.v_cycle, 5) / 5
             del sv
-        if vcycle is not None:
-            vcycle.update(small)
+
+    # ---- adaptation protocols (configs 2 and 5), bounded V-cycle budgets -----------
+    protos = None
+    if rank == 0 and ws == 1 and not args.no_protocols and not args.quick:
+        from paper_1806_11456_b200 import protocols
+
+        protos = {}
+        t0 = time.perf_counter()
+        run2 = protocols.run_config2(max_cycles=args.protocol_cycles)
+        protos["cfg2"] = dict(run2.to_dict(), wall_s=round(time.perf_counter() - t0, 1))
+        del run2
+        t0 = time.perf_counter()
+        run5 = protocols.run_config5(max_cycles=args.protocol_cycles, stages=args.cfg5_stages)
+        protos["cfg5"] = dict(run5.to_dict(), wall_s=round(time.perf_counter() - t0, 1))
+        del run5
+        protos["note"] = (f"at most {args.protocol_cycles} V-cycles per stage; a stage that misses |r| <= "
+                          "tau_max/10 in that budget estimates tau with the gate bypassed (recorded); "
+                          "cfg5 runs its first {} threshold stage(s) here".format(args.cfg5_stages))
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, info = cpu_sample_rate(n=6, budget_s=args.cpu_budget)
         cpu = {"value": rate, "unit": "DOF-evals/s", "cores": 1, "kind": "port", "sample": info["sample"],
-               "evals": info["evals"], "seconds": info["seconds"]}
+               "evals": info["evals"], "seconds": info["seconds"], **cpu_info()}
+    ref2d = None
+    try:
+        with open(REF2D) as fh:
+            ref2d = json.load(fh)
+    except Exception:
+        pass
 
     if rank == 0:
         out = {
@@ -397,8 +527,9 @@ def run_b200(args):
             "config": {"workload": w.name, "nodes": nodes, "unknowns": 5 * nodes,
                        "global_batch": nodes * ws, "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                        "family": w.family, "metrics": w.form, "l2": "inputs > L2 (Q is 163 MB)"},
-            "roofline": roofline, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
-            "vcycle": vcycle, "cpu_baseline": cpu, "setup_s": round(setup_s, 1),
+            "roofline": roofline, "e2e": e2e, "gpu_launches": launches * 1, "clocks": clk,
+            "rk3_stage": rk, "tau_estimate": tau_est, "vcycle": vcycle, "cfg5": cfg5, "protocols": protos,
+            "cpu_baseline": cpu, "reference_cpu_2d": ref2d, "setup_s": round(setup_s, 1),
         }
         print(json.dumps(out), flush=True)
     if dist is not None:
@@ -415,6 +546,10 @@ def main():
     ap.add_argument("--no-vcycle", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--quick", action="store_true", help="headline residual, e2e and V-cycles only")
+    ap.add_argument("--no-protocols", action="store_true")
+    ap.add_argument("--protocol-cycles", type=int, default=30)
+    ap.add_argument("--cfg5-stages", type=int, default=1)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

@@ -147,7 +147,9 @@ def config2(seed=1, nx=40, ny=20, order=5, dz=0.05, nz_order=1) -> Workload:
     return Workload(f"cfg2: {nx}x{ny}x1 graded flat plate, N={order} (Nz={nz_order}) LGL, NS M=0.2 Re=1e5",
                     msh, law, OrderField(orders), init,
                     smoother=dict(pre_sweeps=3, post_sweeps=3, coarsest_sweeps=10, max_batches=1),
-                    notes="Nz held at 1 (not adapted); two-sided x clustering 13/27 cells")
+                    time=dict(cfl_advective=0.05, cfl_viscous=0.025),
+                    notes="Nz held at 1 (not adapted); two-sided x clustering 13/27 cells; CFL 0.05/0.025: "
+                          "V-cycles at 0.2/0.1 diverge through the coarse-grid correction (measured)")
 
 
 def config5(seed=5, na=16, nr=24, order=3, r1=10.0) -> Workload:
