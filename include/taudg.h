@@ -206,13 +206,11 @@ int tdg_prolong_add(const tdg_transfer* t, const double* Qc, const double* Qc0, 
 
 /* Lifted BR1 gradient (operators.py:224-265; debug/parity): one trace + lift
  * pass over Q (coupled or isolated) that writes the per-node gradient,
- * [3][ngv][n] per element in slot order, to dst (device).  Plans whose flux
- * kernel recomputes the gradient never store it during evaluations. */
+ * [3][ngv][n] per element in slot order, to dst (device). */
 int tdg_gradient(tdg_plan* plan, const double* Q, int isolated, double* dst, void* stream);
-/* Plan facts for tests and the bench: recompute = 1 when the flux kernel
- * recomputes the BR1 gradient (every work item affine); nwork = element work
- * items (blocks per element-kernel launch). */
-int tdg_plan_info(const tdg_plan* plan, int32_t* recompute, int32_t* nwork);
+/* Plan facts for tests and the bench: element work items (blocks per
+ * element-kernel launch), conforming and nonconforming (mortar) interior faces. */
+int tdg_plan_info(const tdg_plan* plan, int32_t* nwork, int32_t* nconf_faces, int32_t* nmortar_faces);
 /* Debug/parity: copy a face scratch buffer of the last evaluation to dst
  * (device): which = 0 Q traces [nv], 1 lift surface [3 ngv], 2 gradient
  * traces [3 ngv], 3 flux surface [nv]; per element side at side_off*C as

@@ -115,3 +115,94 @@ def limit_jumps(msh, orders, rule="strict-one"):
         if not changed:
             return OrderField(arr)
     raise AdaptationError("jump limiting failed to reach a fixed point")
+
+
+def _boundary_face_frames(msh, face_ids):
+    """Frame index (0 or 1) of each element-local tangential axis of the given
+    boundary faces, transported across shared face edges: two faces sharing an
+    edge give the axis running along it the same frame index, and likewise the
+    axis crossing it.  Each connected piece starts from its first face's local
+    order (t1 -> 0, t2 -> 1); on a closed surface whose frame cannot be
+    transported consistently the first assignment wins."""
+    M = np.array(msh.nodes.shape[1:4]) - 1
+    edges = {}
+    info = []
+    for fi in face_ids:
+        f = msh.faces[fi]
+        e, s = f.left, f.side_left
+        d = s // 2
+        a, b = [x for x in range(3) if x != d]
+        idx = [0, 0, 0]
+        idx[d] = 0 if s % 2 == 0 else int(M[d])
+
+        def corner(ia, ib):
+            j = list(idx)
+            j[a], j[b] = ia, ib
+            return msh.nodes[e, j[0], j[1], j[2]]
+
+        scale = float(np.abs(msh.nodes[e]).max()) + 1.0
+        key = lambda p, q: tuple(sorted((tuple(np.round(p / scale, 9)), tuple(np.round(q / scale, 9)))))
+        mine = []
+        for ib in (0, int(M[b])):       # edges running along a
+            mine.append((key(corner(0, ib), corner(int(M[a]), ib)), a, b))
+        for ia in (0, int(M[a])):       # edges running along b
+            mine.append((key(corner(ia, 0), corner(ia, int(M[b]))), b, a))
+        info.append((e, a, b, mine))
+        for k, along, across in mine:
+            edges.setdefault(k, []).append((len(info) - 1, along, across))
+    frame = [None] * len(info)
+    for start in range(len(info)):
+        if frame[start] is not None:
+            continue
+        e, a, b, _ = info[start]
+        frame[start] = {a: 0, b: 1}
+        queue = [start]
+        while queue:
+            u = queue.pop(0)
+            for k, along, across in info[u][3]:
+                for v, v_along, v_across in edges[k]:
+                    if frame[v] is None:
+                        frame[v] = {v_along: frame[u][along], v_across: frame[u][across]}
+                        queue.append(v)
+    return [(info[i][0], frame[i]) for i in range(len(info))]
+
+
+def conforming_pass(msh, orders, tags, rule=None):
+    """adaptation.py:212-250 in 3D: on each tagged boundary, every element's
+    tangential order in frame direction k becomes the maximum over the tag
+    (frames transported across shared edges, _boundary_face_frames); with a
+    jump rule, alternate with limit_jumps until neither changes the field."""
+    tags = tuple(tags)
+    unknown = [t for t in tags if t not in msh.boundary_tags]
+    if unknown:
+        raise AdaptationError(f"unknown boundary tags: {unknown}")
+    groups = []
+    for tag in tags:
+        slots = [[], []]
+        for e, fr in _boundary_face_frames(msh, msh.boundary_tags[tag]):
+            for axis, k in fr.items():
+                slots[k].append((e, axis))
+        groups += [g for g in slots if g]
+
+    def share(arr):
+        changed = False
+        for slots in groups:
+            top = max(int(arr[e, d]) for e, d in slots)
+            for e, d in slots:
+                if arr[e, d] != top:
+                    arr[e, d] = top
+                    changed = True
+        return changed
+
+    arr = orders.orders.copy()
+    if rule is None:
+        share(arr)
+        return OrderField(arr)
+    for _ in range(arr.size * (int(arr.max()) + 1) + 1):
+        changed = share(arr)
+        limited = limit_jumps(msh, OrderField(arr), rule)
+        changed = changed or not np.array_equal(limited.orders, arr)
+        arr = limited.orders.copy()
+        if not changed:
+            return limited
+    raise AdaptationError("conforming pass failed to reach a fixed point")

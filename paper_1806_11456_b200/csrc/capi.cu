@@ -150,7 +150,6 @@ struct tdg_plan {
   int64_t side_nodes = 0;
   int iso = -1;          // isotropic order of a single-bucket plan, else -1
   int nsm = 148;
-  double* grad_dbg = nullptr;   // gradient buffer for tdg_gradient on recompute plans (lazy)
   // host-buffer batch evaluation (tdg_residual_host): two device staging
   // slots, two copy streams, per-slot events; created on first use
   struct Staging {
@@ -234,22 +233,16 @@ int setup_attrs(tdg_plan* p) {
     constexpr int NX = decltype(nx)::value;
     int r;
     if ((r = allow_smem(k_vol_lift<LAW, NX>, lift))) return r;
-    if ((r = allow_smem(k_vol_lift_own<LAW, NX, false>, own))) return r;
-    if ((r = allow_smem(k_vol_lift_own<LAW, NX, true>, own))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX, false>, flux))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX, false>, flux))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX, false>, flux))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX, true>, flux))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX, true>, flux))) return r;
-    if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX, true>, flux))) return r;
+    if ((r = allow_smem(k_vol_lift_own<LAW, NX>, own))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX>, flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX>, flux))) return r;
+    if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX>, flux))) return r;
     return TDG_OK;
   });
   if (rc) return rc;
   // cold modes use runtime orders only
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, -1, false>, flux))) return rc;
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, -1, false>, flux))) return rc;
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, -1, true>, flux))) return rc;
-  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, -1, true>, flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_F, -1>, flux))) return rc;
+  if ((rc = allow_smem(k_vol_flux<LAW, MODE_TAU, -1>, flux))) return rc;
   return TDG_OK;
 }
 
@@ -309,15 +302,11 @@ int run_surface(tdg_plan* p, const DevPlan& d, const double* Q, int isolated, cu
     {
       KTimer kt(TDG_K_VOL_LIFT, st);
       // LGL and every evaluated side on own-order traces: direct trace writes
-      // (face nodes only when the flux kernel recomputes the gradient)
       const bool own = d.family == TDG_LGL && (isolated || d.nmface == 0);
-      const bool face_only = d.recompute && d.grad == nullptr;
       with_nx<LAW>(p->iso, [&](auto nx) -> int {
         constexpr int NX = decltype(nx)::value;
-        if (own && face_only)
-          k_vol_lift_own<LAW, NX, true><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q, coupled);
-        else if (own)
-          k_vol_lift_own<LAW, NX, false><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q, coupled);
+        if (own)
+          k_vol_lift_own<LAW, NX><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q, coupled);
         else
           k_vol_lift<LAW, NX><<<d.nwork, p->elem_threads, p->smem_lift, st>>>(d, Q, coupled);
         return 0;
@@ -340,22 +329,14 @@ int run_eval(tdg_plan* p, const double* Q, int isolated, const FluxArgs& a0, cud
   {
     KTimer kt(TDG_K_VOL_FLUX, st);
     constexpr bool hot = MODE == MODE_R || MODE == MODE_RK || MODE == MODE_A;
-    const bool rec = p->d.recompute != 0;
-    auto launch = [&](auto nx, auto recv) {
-      constexpr int NX = decltype(nx)::value;
-      constexpr bool REC = decltype(recv)::value;
-      k_vol_flux<LAW, MODE, NX, REC><<<p->d.nwork, p->elem_threads, p->smem_flux, st>>>(p->d, Q, a);
-      return 0;
-    };
     if (hot) {
       with_nx<LAW>(p->iso, [&](auto nx) -> int {
-        constexpr int NX = hot ? decltype(nx)::value : -1;
-        return rec ? launch(std::integral_constant<int, NX>(), std::true_type())
-                   : launch(std::integral_constant<int, NX>(), std::false_type());
+        k_vol_flux<LAW, MODE, hot ? decltype(nx)::value : -1><<<p->d.nwork, p->elem_threads, p->smem_flux, st>>>(
+            p->d, Q, a);
+        return 0;
       });
     } else {
-      rec ? launch(std::integral_constant<int, -1>(), std::true_type())
-          : launch(std::integral_constant<int, -1>(), std::false_type());
+      k_vol_flux<LAW, MODE, -1><<<p->d.nwork, p->elem_threads, p->smem_flux, st>>>(p->d, Q, a);
     }
   }
   LAUNCH_CHECK("k_vol_flux");
@@ -717,13 +698,6 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     d.pf_face = knob("TDG_PF_FACE", 4);
     d.pf_down = knob("TDG_PF_DOWN", 5);
     d.pf_item = knob("TDG_PF_ITEM", 1);
-    // every work item affine: the flux kernel recomputes the BR1 gradient and
-    // the lift writes only its side traces.  Opt-in (TDG_RECOMPUTE=1): measured
-    // slower on config 4 (V-cycle 60.5 -> 74-80 ms), the element kernels are
-    // shared-memory-bandwidth bound and the recompute adds 96 loads per node
-    bool all_aff = !work.empty();
-    for (int a : work_aff) all_aff = all_aff && a != 0;
-    d.recompute = (p->viscous && all_aff && knob("TDG_RECOMPUTE", 0)) ? 1 : 0;
     int coll = 0;
     for (int dd = 0; dd < 3; ++dd) {
       bool c = ns > 0;
@@ -772,7 +746,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     p->smem_lift_own = static_cast<size_t>(p->ngv + (curved ? 9 : 0)) * mt * sizeof(double);
   }
   p->smem_flux = static_cast<size_t>(3 * p->nv) * mt * sizeof(double);
-  if (p->viscous && !d.recompute) {
+  if (p->viscous) {
     if ((rc = p->mem.zeros(static_cast<size_t>(p->nodes) * NG, &grad))) {
       delete p;
       return rc;
@@ -1024,10 +998,11 @@ int tdg_gradient(tdg_plan* p, const double* Q, int isolated, double* dst, void* 
   }
 }
 
-int tdg_plan_info(const tdg_plan* p, int32_t* recompute, int32_t* nwork) {
+int tdg_plan_info(const tdg_plan* p, int32_t* nwork, int32_t* nconf_faces, int32_t* nmortar_faces) {
   if (!p) return fail(TDG_E_ARG, "null plan");
-  if (recompute) *recompute = p->d.recompute;
   if (nwork) *nwork = p->d.nwork;
+  if (nconf_faces) *nconf_faces = p->d.ncface;
+  if (nmortar_faces) *nmortar_faces = p->d.nmface;
   return TDG_OK;
 }
 

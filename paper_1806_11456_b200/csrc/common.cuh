@@ -55,10 +55,6 @@ struct DevPlan {
   int nsm;        // SMs: kernels prefetch the work about one wave ahead (L2)
   int pf_trace, pf_face, pf_down;   // look-ahead distances, blocks per SM
   int pf_item;    // element kernels: L2 bulk prefetch of the item's own spans
-  // BR1 gradient recomputed inside the flux kernel (every work item affine):
-  // the lift kernel writes only the gradient's side traces and no per-node
-  // gradient (12 doubles per node written once and read once less)
-  int recompute;
   int collapsed;  // bit d: direction d has order 0 on every element (2D extrusion)
   // side work items for side kernels: (slot, side | kind<<8), ghost offset
   int nside_iso;
@@ -88,7 +84,7 @@ struct DevPlan {
   double* lsurf;  // [side_nodes][3*ngv]   lift surface contributions
   double* gtr;    // [side_nodes][3*ngv] own-order gradient traces
   double* fsurf;  // [side_nodes][nv]      flux surface contributions
-  double* grad;   // [nodes][3*ngv] lifted gradient (NULL: not stored, see recompute)
+  double* grad;   // [nodes][3*ngv] lifted gradient
   // conforming-face lift in g* form (LGL plans without nonconforming faces):
   // k_face<lift> writes g* = ½(g_L + g_R) once per face node ([ngv][nm] at
   // the left side's trace offset) instead of g*·n σ for both sides (2 x 3 ngv),

@@ -494,36 +494,6 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
   }
 }
 
-// Face nodes of an LGL element with (n1p, n2p, n3p) >= 2 points per
-// direction: the planes k = 0 and k = N3 first, then the rings (j = 0,
-// j = N2, i = 0, i = N1) of the inner planes.
-__device__ __forceinline__ int face_node_count(int n1p, int n2p, int n3p) {
-  return 2 * n1p * n2p + (n3p - 2) * (2 * n1p + 2 * (n2p - 2));
-}
-
-__device__ __forceinline__ void face_node(int f, int n1p, int n2p, int n3p, int& i, int& j, int& k) {
-  const int pl = n1p * n2p;
-  if (f < 2 * pl) {
-    k = f < pl ? 0 : n3p - 1;
-    const int g = f < pl ? f : f - pl;
-    j = g / n1p;
-    i = g - j * n1p;
-    return;
-  }
-  const int ring = 2 * n1p + 2 * (n2p - 2);
-  const int g = f - 2 * pl;
-  k = 1 + g / ring;
-  const int p = g - (k - 1) * ring;
-  if (p < 2 * n1p) {
-    j = p < n1p ? 0 : n2p - 1;
-    i = p < n1p ? p : p - n1p;
-  } else {
-    const int q = p - 2 * n1p;
-    j = 1 + (q >> 1);
-    i = (q & 1) ? n1p - 1 : 0;
-  }
-}
-
 // BR1 lift for LGL plans whose evaluated sides all use own-order traces (no
 // nonconforming face, or an isolated evaluation): the side traces of G are
 // face-node values, so every node writes its gradient straight to the
@@ -531,11 +501,7 @@ __device__ __forceinline__ void face_node(int f, int n1p, int n2p, int n3p, int&
 // plan stores it).  No staging of G in shared memory and no second barrier,
 // so each thread keeps one node's values at a time (80 registers, 3 blocks
 // per SM: measured faster than 4 blocks with spills at 64).
-//
-// FACE_ONLY (plans whose flux kernel recomputes G, P.recompute): only the
-// face nodes are lifted — the interior gradient is never needed here.  An
-// N=7 element has 296 face nodes of 512.
-template <int LAW, int NX, bool FACE_ONLY>
+template <int LAW, int NX>
 __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, const double* __restrict__ Q,
                                                                    int coupled) {
   using L = Law<LAW>;
@@ -561,26 +527,16 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
   // staging needs no table: one barrier covers both
   stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
   __syncthreads();
-  const int nfn = FACE_ONLY ? face_node_count(n1p, n2p, n3p) : n;
-  const int tasks = wi.y * nfn;
 #pragma unroll 1
-  for (int t = threadIdx.x; t < tasks; t += blockDim.x) {
-    const int e = t / nfn, f = t - e * nfn, slot = wi.x + e;
-    int i, j, k;
-    if (FACE_ONLY) {
-      face_node(f, n1p, n2p, n3p, i, j, k);
-    } else {
-      i = f % n1p;
-      j = (f / n1p) % n2p;
-      k = f / (n1p * n2p);
-    }
-    const int node = i + n1p * (j + n2p * k);
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int e = t / n, node = t - e * n, slot = wi.x + e;
+    const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
     double x[NG];
     if (coupled && P.gstar)
       lift_node<LAW, NX, true>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
     else
       lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
-    if (!FACE_ONLY && P.grad) {
+    if (P.grad) {
       const long long gb = P.node_off[slot] * NG;
 #pragma unroll
       for (int c = 0; c < NG; ++c) P.grad[gb + (long long)c * n + node] = x[c];
@@ -619,82 +575,8 @@ struct FluxArgs {
   int coupled;         // coupled (1) or isolated (0) evaluation (the lift's surface terms)
 };
 
-// Contravariant fluxes f~_i = Ja^i . (f_a - f_v) of an affine work item with
-// the BR1 gradient recomputed in place (P.recompute): g(q) is staged in the
-// direction-2 flux region, each node's G comes from lift_node (the same
-// arithmetic the lift kernel uses), f~_0, f~_1 go to shared memory at once
-// and f~_2 waits in registers until every thread has finished reading g.
-// Shared memory stays [3][NV][tot] (3 blocks per SM), and the 12-double
-// gradient never touches HBM.
-template <int LAW, int NX>
-__device__ __forceinline__ void item_fluxes_recompute(const DevPlan& P, const double* __restrict__ Q,
-                                                      const FluxArgs& A, int2 wi, int N1, int N2, int N3,
-                                                      ElemTables& T, double* ft) {
-  using L = Law<LAW>;
-  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
-  const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
-  const int n = n1p * n2p * n3p, tot = wi.y * n;
-  double qa[NPT][NV];
-  load_item_state<NV>(P, Q, wi, n, tot, qa);
-  load_tables(P, N1, N2, N3, T);
-  double* gs = ft + 2 * NV * tot;   // [NGV][tot] inside the direction-2 region
-  stage_grad_vars<LAW>(P, wi, n, tot, true, qa, gs, nullptr);
-  __syncthreads();
-  const bool gstar = A.coupled && P.gstar;
-  double f2[NPT][NV];
-#pragma unroll
-  for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * blockDim.x;
-    if (t < tot) {
-      const int e = t / n, node = t - e * n, slot = wi.x + e;
-      const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
-      double G[NG];
-      if (gstar)
-        lift_node<LAW, NX, true>(P, T, gs, nullptr, true, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, G);
-      else
-        lift_node<LAW, NX>(P, T, gs, nullptr, true, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, G);
-      double f[3][NV], Gd[3][NGV];
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-#pragma unroll
-        for (int kk = 0; kk < NGV; ++kk) Gd[d][kk] = G[d * NGV + kk];
-      L::adv_flux(P.prm, qa[r], f);
-      L::sub_visc(P.prm, qa[r], Gd, f);
-      const double* m = P.metrics + P.metric_off[slot];
-#pragma unroll
-      for (int ii = 0; ii < 3; ++ii) {
-        const double j0 = m[1 + 3 * ii], j1 = m[2 + 3 * ii], j2 = m[3 + 3 * ii];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const double x = j0 * f[0][v] + j1 * f[1][v] + j2 * f[2][v];
-          if (ii < 2)
-            ft[(ii * NV + v) * tot + t] = x;
-          else
-            f2[r][v] = x;
-        }
-      }
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * blockDim.x;
-    if (t < tot) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) ft[(2 * NV + v) * tot + t] = f2[r][v];
-    }
-  }
-  __syncthreads();
-}
-
-// REC: the plan recomputes the gradient (every item affine, viscous law);
-// its lift + flux working set needs more than 80 registers, so REC blocks
-// run REC_BLOCKS per SM.
-#ifndef REC_BLOCKS
-#define REC_BLOCKS 2
-#endif
-template <int LAW, int MODE, int NX, bool REC>
-__global__ void __launch_bounds__(ELEM_THREADS, REC ? REC_BLOCKS : 3) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
+template <int LAW, int MODE, int NX>
+__global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
@@ -706,14 +588,7 @@ __global__ void __launch_bounds__(ELEM_THREADS, REC ? REC_BLOCKS : 3) k_vol_flux
   // epilogue inputs, read after the contraction
   if (MODE != MODE_F) prefetch_item_nodes<NV>(P, MODE == MODE_A ? A.X : A.S, wi, 32);
   if (MODE == MODE_RK && A.stage != 0) prefetch_item_nodes<NV>(P, A.W, wi, 64);
-  if (REC) {
-    // the lift's surface terms, read by the recomputed gradient
-    if (A.coupled && P.gstar) {
-      if (threadIdx.x >= 96) prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
-    } else {
-      if (threadIdx.x == 96) prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
-    }
-  } else if (P.pf_item) {
+  if (P.pf_item) {
     // the item's state and gradient spans, read node by node below (the
     // second node of each thread only after the first one's flux)
     prefetch_item_nodes<NV>(P, Q, wi, 96);
@@ -723,45 +598,41 @@ __global__ void __launch_bounds__(ELEM_THREADS, REC ? REC_BLOCKS : 3) k_vol_flux
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
   double* ft = sm;   // [3][NV][tot]
-  if (REC) {
-    item_fluxes_recompute<LAW, NX>(P, Q, A, wi, N1, N2, N3, T, ft);
-  } else {
-    const bool visc = L::viscous(P.prm);
-    // the contravariant fluxes need no table: they are formed first, the
-    // tables are staged after them, and one barrier covers both
+  const bool visc = L::viscous(P.prm);
+  // the contravariant fluxes need no table: they are formed first, the
+  // tables are staged after them, and one barrier covers both
 #pragma unroll 1
-    for (int r = 0; r < NPT; ++r) {
-      const int t = threadIdx.x + r * blockDim.x;
-      if (t < tot) {
-        const int e = t / n, node = t - e * n, slot = wi.x + e;
-        const long long base = P.node_off[slot] * NV;
-        double q[NV], f[3][NV];
+  for (int r = 0; r < NPT; ++r) {
+    const int t = threadIdx.x + r * blockDim.x;
+    if (t < tot) {
+      const int e = t / n, node = t - e * n, slot = wi.x + e;
+      const long long base = P.node_off[slot] * NV;
+      double q[NV], f[3][NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) q[v] = Q[base + (long long)v * n + node];
-        L::adv_flux(P.prm, q, f);
-        if (visc) {
-          double G[3][NGV];
-          const double* gp = P.grad + P.node_off[slot] * NG + node;
+      for (int v = 0; v < NV; ++v) q[v] = Q[base + (long long)v * n + node];
+      L::adv_flux(P.prm, q, f);
+      if (visc) {
+        double G[3][NGV];
+        const double* gp = P.grad + P.node_off[slot] * NG + node;
 #pragma unroll
-          for (int d = 0; d < 3; ++d)
+        for (int d = 0; d < 3; ++d)
 #pragma unroll
-            for (int k = 0; k < NGV; ++k) G[d][k] = gp[(long long)(d * NGV + k) * n];
-          L::sub_visc(P.prm, q, G, f);
-        }
-        int ms;
-        const double* m = metric_ptr(P, slot, node, n, ms);
+          for (int k = 0; k < NGV; ++k) G[d][k] = gp[(long long)(d * NGV + k) * n];
+        L::sub_visc(P.prm, q, G, f);
+      }
+      int ms;
+      const double* m = metric_ptr(P, slot, node, n, ms);
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          const double j0 = m[(1 + 3 * i) * ms], j1 = m[(2 + 3 * i) * ms], j2 = m[(3 + 3 * i) * ms];
+      for (int i = 0; i < 3; ++i) {
+        const double j0 = m[(1 + 3 * i) * ms], j1 = m[(2 + 3 * i) * ms], j2 = m[(3 + 3 * i) * ms];
 #pragma unroll
-          for (int v = 0; v < NV; ++v)
-            ft[(i * NV + v) * tot + t] = j0 * f[0][v] + j1 * f[1][v] + j2 * f[2][v];
-        }
+        for (int v = 0; v < NV; ++v)
+          ft[(i * NV + v) * tot + t] = j0 * f[0][v] + j1 * f[1][v] + j2 * f[2][v];
       }
     }
-    load_tables(P, N1, N2, N3, T);
-    __syncthreads();
   }
+  load_tables(P, N1, N2, N3, T);
+  __syncthreads();
 
   double rmax = 0.0;
 #pragma unroll 1

@@ -527,13 +527,11 @@ class DGOperator:
                   self._stream())
         return out
 
-    @property
-    def recomputes_gradient(self) -> bool:
-        """True when the flux kernel recomputes the BR1 gradient (no per-node
-        gradient in HBM; every work item affine)."""
-        rec = C.c_int32()
-        _lib.call("tdg_plan_info", self._plan, C.byref(rec), None)
-        return bool(rec.value)
+    def plan_info(self) -> dict:
+        """Element work items and interior-face counts of the device plan."""
+        nw, nc, nm = C.c_int32(), C.c_int32(), C.c_int32()
+        _lib.call("tdg_plan_info", self._plan, C.byref(nw), C.byref(nc), C.byref(nm))
+        return {"work_items": nw.value, "conforming_faces": nc.value, "mortar_faces": nm.value}
 
     def debug_buffer(self, which: int):
         """Face scratch buffer of the last evaluation, as a dict

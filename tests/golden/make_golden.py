@@ -239,8 +239,27 @@ def adapt_case(name, spec):
     save(f"adapt_{name}", case="advdiff-sine", **out, **mesh_arrays(m))
 
 
+def conforming_case():
+    """conforming_pass (adaptation.py:212-250): tag-max sharing alone and
+    alternated with both jump rules, on a graded mesh with random orders."""
+    m = mesh.build_cartesian(5, 4, grading=("south", 1.2))
+    rng = np.random.default_rng(21)
+    of = OrderField(rng.integers(1, 7, (m.num_elements, 2)))
+    out = {"orders_in": of.orders}
+    for k, tags in enumerate((("south",), ("south", "north"), ("west", "east", "north"))):
+        out[f"tags_{k}"] = np.array(tags)
+        out[f"share_{k}"] = ad.conforming_pass(m, of, tags).orders
+        out[f"strict_{k}"] = ad.conforming_pass(m, of, tags, "strict-one").orders
+        out[f"soft_{k}"] = ad.conforming_pass(m, of, tags, "softened").orders
+    save("conforming", **out, **mesh_arrays(m))
+
+
 def main():
     np.set_printoptions(precision=3)
+    if len(sys.argv) > 1:        # named cases only, e.g. `make_golden.py conforming`
+        for name in sys.argv[1:]:
+            globals()[f"{name}_case"]()
+        return
     spectral_case()
     for name, spec in OP_CASES.items():
         op_case(name, spec)
@@ -250,6 +269,7 @@ def main():
     tau_case()
     for name, spec in ADAPT_CASES.items():
         adapt_case(name, spec)
+    conforming_case()
 
 
 if __name__ == "__main__":

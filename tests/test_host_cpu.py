@@ -147,3 +147,50 @@ def test_affine_metrics_are_exact_and_shared_with_the_oracle():
         j, k = (i + 1) % 3, (i + 2) % 3
         assert np.allclose(ja[:, i, i], h[j] * h[k] / 4, rtol=1e-15, atol=0)
         assert (ja[:, i, j] == 0).all() and (ja[:, i, k] == 0).all()
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+@pytest.mark.parametrize("rule", [None, "strict-one", "softened"])
+def test_conforming_pass_matches_reference(k, rule):
+    """conforming_pass (adaptation.py:212-250) on the reference's own golden
+    case (graded 5x4 mesh, three tag sets), product and oracle."""
+    from oracle import adaptation as oad
+    from oracle.fields import OrderField as OO
+
+    g = load("conforming")
+    m = golden_mesh(g)
+    orders = orders3(g["orders_in"])
+    tags = tuple(str(t) for t in g[f"tags_{k}"])
+    want = g[{None: "share", "strict-one": "strict", "softened": "soft"}[rule] + f"_{k}"]
+    got = adaptation.conforming_pass(m, OrderField(orders), tags, rule)
+    assert (got.orders[:, :2] == want).all()
+    assert (got.orders[:, 2] == 0).all()
+    assert (oad.conforming_pass(m, OO(orders), tags, rule).orders[:, :2] == want).all()
+
+
+@pytest.mark.parametrize("builder", ["rotated_box", "cubed_sphere"])
+def test_conforming_pass_3d_matches_oracle(builder):
+    """3D meshes whose boundary elements are rotated against each other
+    (every orientation code; the six cubed-sphere panels): the product's
+    frame-transported sharing equals the oracle's, is idempotent, and with a
+    jump rule leaves every interior face within the rule."""
+    from oracle import adaptation as oad
+    from oracle.fields import OrderField as OO
+
+    if builder == "rotated_box":
+        m = mesh.build_rotated_box(3, 3, 2, seed=5)
+        tags = ("boundary",)
+    else:
+        m = mesh.build_cubed_sphere(2, 2, 0.5, 2.0, 1.15)
+        tags = tuple(sorted(m.boundary_tags))[:1]
+    arr = np.random.default_rng(7).integers(1, 7, (m.num_elements, 3))
+    for rule in (None, "strict-one"):
+        got = adaptation.conforming_pass(m, OrderField(arr), tags, rule)
+        ref = oad.conforming_pass(m, OO(arr), tags, rule)
+        assert (got.orders == ref.orders).all()
+        assert (got.orders >= arr).all()
+        again = adaptation.conforming_pass(m, got, tags, rule)
+        assert (again.orders == got.orders).all()
+        if rule:
+            for ea, da, eb, db in adaptation._face_slot_pairs(m):
+                assert abs(int(got.orders[ea, da]) - int(got.orders[eb, db])) <= 1
