@@ -217,6 +217,24 @@ int tdg_plan_info(const tdg_plan* plan, int32_t* nwork, int32_t* nconf_faces, in
  * [C][nf] with t1 fastest.  Returns the element count in *len_out. */
 int tdg_debug_copy(tdg_plan* plan, int which, double* dst, int64_t* len_out, void* stream);
 
+/* Device-resident tuned smoothing (multigrid.py:254-301):
+ * a WHILE conditional node inside a CUDA-graph stream capture.
+ * tdg_loop_begin, on a capturing `stream`, appends the node and starts
+ * capturing its body on the caller's idle `body_stream` (issue the body's
+ * work there); tdg_loop_test appends the end-of-batch test that
+ * sets the loop condition: count += 1, floor = max(1e-13 max(1, *snorm),
+ * *tolf); stop if *rnorm <= floor, or (mode 0, pre-smoothing) *rnorm <
+ * eta * *cmp or *cmp == 0, or (mode 1, post-smoothing) *rnorm <= *cmp; the
+ * body repeats while not stopped and count < max_iter (it always runs once).
+ * tdg_loop_end closes the body capture and frees the handle object. */
+typedef struct tdg_loop tdg_loop;
+/* A private non-blocking stream for loop bodies (created outside any capture). */
+int tdg_stream_create(void** stream_out);
+int tdg_stream_destroy(void* stream);
+int tdg_loop_begin(void* stream, void* body_stream, tdg_loop** out);
+int tdg_loop_test(tdg_loop* loop, const double* rnorm, const double* snorm, const double* tolf,
+                  const double* cmp, double eta, int mode, int32_t* count, int max_iter);
+int tdg_loop_end(tdg_loop* loop);
 /* Per-kernel timing (process-wide): when enabled, every kernel launch made
  * through this library is bracketed by CUDA events on its own stream.
  * tdg_timing_read synchronises the recorded events, writes the summed

@@ -64,6 +64,11 @@ SIGNATURES = {
     "tdg_prolong": ([_VP, _VP, _VP, _VP], C.c_int),
     "tdg_prolong_add": ([_VP, _VP, _VP, _VP, _VP], C.c_int),
     "tdg_gradient": ([_VP, _VP, C.c_int, _VP, _VP], C.c_int),
+    "tdg_loop_begin": ([_VP, _VP, C.POINTER(_VP)], C.c_int),
+    "tdg_loop_test": ([_VP, _VP, _VP, _VP, _VP, _dbl, C.c_int, _VP, C.c_int], C.c_int),
+    "tdg_loop_end": ([_VP], C.c_int),
+    "tdg_stream_create": ([C.POINTER(_VP)], C.c_int),
+    "tdg_stream_destroy": ([_VP], C.c_int),
     "tdg_plan_info": ([_VP, _pi32, _pi32, _pi32], C.c_int),
     "tdg_tau_from_avalue": ([_VP, _VP, _VP, _VP, _VP], C.c_int),
     "tdg_debug_copy": ([_VP, C.c_int, _VP, _pi64, _VP], C.c_int),

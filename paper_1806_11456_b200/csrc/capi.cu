@@ -121,6 +121,25 @@ struct KTimer {
 const char* const KNAMES[TDG_K_COUNT] = {"trace_q", "side_lift", "face_lift", "vol_lift", "side_flux",
                                          "face_flux", "vol_flux", "element_dt", "norm", "transfer", "mortar_face", "up_proj"};
 
+// End-of-batch test of a tuned smoothing phase (multigrid.py:254-301), on the
+// device: floor = max(1e-13 max(1, |S|), tol floor); pre-smoothing stops at
+// |r| <= floor or |r| < eta |I r| (or |I r| = 0), post-smoothing at |r| <=
+// floor or |r| <= the pre-smoothing norm; the loop also stops after max_iter
+// batches.  Sets the enclosing WHILE node's condition.
+__global__ void k_loop_test(cudaGraphConditionalHandle h, const double* rnorm, const double* snorm,
+                            const double* tolf, const double* cmp, double eta, int mode, int* count,
+                            int max_iter) {
+  const int c = ++(*count);
+  const double rn = *rnorm;
+  const double fl = fmax(1e-13 * fmax(1.0, *snorm), *tolf);
+  bool stop = rn <= fl;
+  if (!stop) {
+    const double cv = *cmp;
+    stop = mode == 0 ? (rn < eta * cv || cv == 0.0) : (rn <= cv);
+  }
+  cudaGraphSetConditional(h, (!stop && c < max_iter) ? 1u : 0u);
+}
+
 __global__ void k_fill(double* p, double v, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -181,6 +200,13 @@ struct tdg_plan {
       }
     }
   } stage;
+};
+
+// A WHILE conditional node being captured (tdg_loop_*): its body graph is
+// captured on a private stream while the outer capture waits on the node.
+struct tdg_loop {
+  cudaGraphConditionalHandle handle{};
+  cudaStream_t body = nullptr;
 };
 
 struct tdg_transfer {
@@ -1023,6 +1049,70 @@ int tdg_debug_copy(tdg_plan* p, int which, double* dst, int64_t* len_out, void* 
   if (!dst) return TDG_OK;
   if (!src) return fail(TDG_E_CONFIG, "buffer not allocated (inviscid plan)");
   CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, as_stream(stream)));
+  return TDG_OK;
+}
+
+int tdg_loop_begin(void* stream, void* body_stream, tdg_loop** out) {
+  if (!out || !body_stream) return fail(TDG_E_ARG, "null argument");
+  cudaStream_t st = as_stream(stream);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CUDA_TRY(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  if (cs != cudaStreamCaptureStatusActive) return fail(TDG_E_ARG, "tdg_loop_begin: stream is not capturing");
+  auto* lp = new tdg_loop();
+  cudaGraphNodeParams prm = {};
+  cudaGraphNode_t node = nullptr;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&lp->handle, g, 1u, cudaGraphCondAssignDefault);
+  if (e == cudaSuccess) {
+    prm.type = cudaGraphNodeTypeConditional;
+    prm.conditional.handle = lp->handle;
+    prm.conditional.type = cudaGraphCondTypeWhile;
+    prm.conditional.size = 1;
+    e = cudaGraphAddNode(&node, g, deps, nd, &prm);
+  }
+  if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies);
+  lp->body = as_stream(body_stream);
+  if (e == cudaSuccess)
+    e = cudaStreamBeginCaptureToGraph(lp->body, prm.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeRelaxed);
+  if (e != cudaSuccess) {
+    delete lp;
+    return fail(TDG_E_CUDA, std::string("tdg_loop_begin: ") + cudaGetErrorString(e));
+  }
+  *out = lp;
+  return TDG_OK;
+}
+
+int tdg_stream_create(void** out) {
+  if (!out) return fail(TDG_E_ARG, "null argument");
+  cudaStream_t s = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = s;
+  return TDG_OK;
+}
+
+int tdg_stream_destroy(void* stream) {
+  if (stream) CUDA_TRY(cudaStreamDestroy(as_stream(stream)));
+  return TDG_OK;
+}
+
+int tdg_loop_test(tdg_loop* lp, const double* rnorm, const double* snorm, const double* tolf, const double* cmp,
+                  double eta, int mode, int32_t* count, int max_iter) {
+  if (!lp || !rnorm || !snorm || !tolf || !cmp || !count) return fail(TDG_E_ARG, "null argument");
+  k_loop_test<<<1, 1, 0, lp->body>>>(lp->handle, rnorm, snorm, tolf, cmp, eta, mode, reinterpret_cast<int*>(count),
+                                      max_iter);
+  LAUNCH_CHECK("k_loop_test");
+  return TDG_OK;
+}
+
+int tdg_loop_end(tdg_loop* lp) {
+  if (!lp) return fail(TDG_E_ARG, "null loop");
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(lp->body, &g);
+  delete lp;
+  if (e != cudaSuccess) return fail(TDG_E_CUDA, std::string("tdg_loop_end: ") + cudaGetErrorString(e));
   return TDG_OK;
 }
 

@@ -319,3 +319,36 @@ def test_line_transfer_kernel_is_bitwise_and_matches_oracle(n_f):
     p = ON(oo_f, t_lin.prolong(Qc).to_oracle_blocks(), 5)
     assert (r - r_o).norm_inf() <= 1e-13 * max(r_o.norm_inf(), 1.0)
     assert (p - p_o).norm_inf() <= 1e-13 * max(p_o.norm_inf(), 1.0)
+
+
+def test_many_small_elements_per_item_match_oracle():
+    """A 2D-extruded (1,1,0) Legendre-Gauss plan with 25,600 four-node
+    elements: work items are capped at MAX_ITEM_ELEMS = 64 elements (the
+    per-element shared-memory reductions of dt, tau and norms), which this
+    plan would otherwise exceed (~86 elements per item).  element_dt, tau
+    (coupled and isolated) and element norms vs the oracle."""
+    from oracle.fields import OrderField as OO
+    from oracle.operators import DGOperator as ODG
+    from oracle import timestep as ots
+    from paper_1806_11456_b200 import fields, mesh, operators, physics, timestep
+
+    msh = mesh.build_box(160, 160, 1, bounds=((0, 1), (0, 1), (0, 0.1)), jitter=0.1,
+                         rng=np.random.default_rng(11))
+    law = physics.make_case("advdiff-sine")
+    orders = np.tile([1, 1, 0], (msh.num_elements, 1))
+    op = operators.DGOperator(msh, law, fields.OrderField(orders), family="LG", form="cross")
+    oo = ODG(msh, oracle_law(law), OO(orders), family="LG", form="cross")
+    Q = op.project_function(lambda x, y, z: 1.0 + 0.5 * np.sin(3 * x + 2 * y) + 0.0 * z)
+    Qo = oo.project_function(lambda x, y, z: 1.0 + 0.5 * np.sin(3 * x + 2 * y) + 0.0 * z)
+    dt, dto = timestep.element_dt(op, Q, timestep.TimeConfig()), ots.element_dt(oo, Qo, ots.TimeConfig())
+    assert np.abs(dt - dto).max() <= 1e-14 * dto.max()
+    for iso in (False, True):
+        # a smooth field on N=1 elements: F = M A is a small difference of
+        # volume and surface terms (measured 7.7e-12 of max tau here), so this
+        # check of the item cap (an overflow corrupts values at O(1)) is
+        # relative to those terms (oracle term_scale)
+        t, to = op.truncation(Q, isolated=iso), oo.truncation(Qo, isolated=iso)
+        scale = max(to.max(), oo.term_scale(Qo, isolated=iso))
+        assert np.abs(t - to).max() <= 1e-12 * scale
+    en = op.element_norms(Q).cpu().numpy()
+    assert np.abs(en - Qo.element_norms_inf()).max() == 0.0

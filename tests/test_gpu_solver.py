@@ -172,3 +172,33 @@ def test_rk_stage_trace_reuse_is_bitwise_identical():
     op.rk3_stage(ref, Wr, op.source, 0, dt_t, False)
     op.rk3_stage(Qb, W, op.source, 0, dt_t, False, fresh=True)
     assert torch.equal(Qb.data, ref.data)
+
+
+def test_tuned_vcycle_graph_matches_eager():
+    """Tuned smoothing (max_batches > 1) replayed as a CUDA graph with WHILE
+    conditional nodes (device-side eta / post <= pre / floor tests, SURVEY
+    §8f.1) reproduces the eager path's log rows, notes, work units and state."""
+    from paper_1806_11456_b200 import configs, multigrid
+
+    w = configs.config1()
+    sm = multigrid.SmootherConfig(pre_sweeps=2, post_sweeps=2, coarsest_sweeps=3, max_batches=4, eta=1.1)
+    runs = []
+    for graphs in (True, False):
+        s = multigrid.FASSolver(w.mesh, w.law, w.orders, smoother=sm, family=w.family, form=w.form)
+        s.use_graphs = graphs
+        s.set_state(s.finest.op.project_function(w.init))
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            for _ in range(3):
+                s.v_cycle()
+            s.converge(0.5 * s.log[-1]["rnorm"], max_cycles=20)
+        assert (s._graph is not None and s._graph.tuned) == graphs
+        runs.append(s)
+    g, e = runs
+    key = lambda s: [(r["level"], r["phase"], r["sweeps"], r["note"]) for r in s.log]
+    assert key(g) == key(e)
+    assert max(r["sweeps"] for r in e.log if r["phase"] in ("pre", "post")) > sm.pre_sweeps   # several batches ran
+    rg, re_ = np.array([r["rnorm"] for r in g.log]), np.array([r["rnorm"] for r in e.log])
+    assert np.abs(rg - re_).max() <= 1e-12 * re_.max()
+    assert g.work_units == pytest.approx(e.work_units, rel=1e-14)
+    assert float((g.Q.data - e.Q.data).abs().max()) <= 1e-12 * float(e.Q.data.abs().max())
