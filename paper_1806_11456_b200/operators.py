@@ -18,7 +18,7 @@ import ctypes as C
 
 import numpy as np
 
-from . import _lib, geometry, spectral
+from . import _lib, compat, geometry, spectral
 from .errors import ConfigError
 from .fields import NodalField, OrderField
 from .mesh import HexMesh
@@ -49,8 +49,11 @@ def _vol_layout(arr):
 class DGOperator:
     """Discrete spatial operator for one (mesh, law, order field) triple."""
 
-    def __init__(self, msh: HexMesh, law, orders: OrderField, family: str = "LGL",
-                 form: str = "curl", device: str = "cuda"):
+    def __init__(self, msh: HexMesh, law, orders: OrderField, family: str | None = None,
+                 form: str | None = None, device: str = "cuda"):
+        # the reference's own 2D mesh / law / (N1, N2) orders are lifted to the
+        # N3 = 0 extrusion with LG nodes and cross metrics (compat.py)
+        msh, law, orders, family, form = compat.resolve(msh, law, orders, family, form)
         if orders.num_elements != msh.num_elements:
             raise ConfigError("order field does not match the mesh element count")
         if family not in spectral.FAMILIES:

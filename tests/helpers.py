@@ -77,3 +77,39 @@ def ref_flat_to_oracle(flatv, of: OOrders, nv=1):
 
 def oracle_to_ref_flat(field: ONodal):
     return np.concatenate([field.element(e).ravel() for e in range(field.field.num_elements)])
+
+
+class RefStyleMesh2D:
+    """Stand-in with the reference Mesh2D's duck type (mesh.py:44-70):
+    ``elements[e].nodes``, ``faces[f].left/side_left/right/side_right/flip``,
+    ``boundary_tags`` — built from a golden case's arrays, so drop-in tests
+    run where the reference package is absent (the GPU box)."""
+
+    class _El:
+        def __init__(self, nodes):
+            self.nodes = nodes
+
+    class _Face:
+        def __init__(self, row):
+            self.left, self.side_left, self.right, self.side_right = (int(v) for v in row[:4])
+            self.flip = bool(row[4])
+
+    def __init__(self, g):
+        self.elements = [self._El(n) for n in g["nodes2d"]]
+        self.faces = [self._Face(r) for r in g["faces2d"]]
+        names = list(g["tag_names"])
+        self.boundary_tags = {str(t): [int(x) for x in g[f"tag_{i}"]] for i, t in enumerate(names)}
+
+
+class RefStyleAdvDiffSine:
+    """The reference's advdiff-sine case (physics.py:94-106) as a 2D law object."""
+
+    name = "advection-diffusion"
+
+    def __init__(self, mu=0.1, velocity=(1.0, 1.0)):
+        self.mu, self.velocity = mu, velocity
+        a, b = velocity
+        pi = np.pi
+        self.exact = lambda x, y: np.sin(pi * x) * np.sin(pi * y)
+        self.source = lambda x, y: (a * pi * np.cos(pi * x) * np.sin(pi * y) + b * pi * np.sin(pi * x) * np.cos(pi * y)
+                                    + 2.0 * mu * pi * pi * np.sin(pi * x) * np.sin(pi * y))

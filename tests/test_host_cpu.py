@@ -194,3 +194,24 @@ def test_conforming_pass_3d_matches_oracle(builder):
         if rule:
             for ea, da, eb, db in adaptation._face_slot_pairs(m):
                 assert abs(int(got.orders[ea, da]) - int(got.orders[eb, db])) <= 1
+
+
+def test_reference_objects_are_lifted_literally():
+    """compat.resolve: the reference's 2D mesh, (N1, N2) orders and 2D law
+    become the N3 = 0 extrusion with LG nodes and cross metrics; 3D inputs keep
+    LGL / curl."""
+    from helpers import RefStyleAdvDiffSine, RefStyleMesh2D
+    from paper_1806_11456_b200 import compat, physics
+
+    g = load("op_sine_warp_mixed")
+    ref_mesh = RefStyleMesh2D(g)
+    hexm, law, of, fam, form = compat.resolve(ref_mesh, RefStyleAdvDiffSine(), g["orders"])
+    assert (fam, form) == ("LG", "cross")
+    assert (of.orders[:, 2] == 0).all() and (of.orders[:, :2] == g["orders"]).all()
+    ext = golden_mesh(g)
+    assert np.array_equal(hexm.nodes, ext.nodes)
+    assert [tuple(a) for a in zip(*hexm.face_arrays())] == [tuple(a) for a in zip(*ext.face_arrays())]
+    assert compat.as_hex_mesh(ref_mesh) is hexm                       # cached
+    assert isinstance(law, physics.AdvectionDiffusion) and law.velocity == (1.0, 1.0, 0.0)
+    assert law.exact(np.array([0.25]), np.array([0.5]), np.array([7.0]))[0] == np.sin(np.pi / 4)
+    assert compat.resolve(ext, law, of)[3:] == ("LGL", "curl")
