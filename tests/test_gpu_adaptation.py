@@ -91,7 +91,8 @@ def _vcycle_tau_select(w, cycles, frozen=()):
                         family=w.family, form=w.form, frozen=frozen)
     nel = w.mesh.num_elements
     vals = [v for e in range(nel) for d in range(3) for v in tmo.tau[e][d].values()]
-    scale = max(max(vals), so.finest.op.term_scale(so.Q, isolated=True))
+    # relative to max(max tau, |M A|_inf)
+    scale = max(max(vals), so.finest.op.apply(so.Q, isolated=True).norm_inf())
     for e in range(nel):
         for d in range(3):
             assert set(tm.tau[e][d]) == set(tmo.tau[e][d])
