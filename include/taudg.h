@@ -204,6 +204,16 @@ int tdg_prolong(const tdg_transfer* t, const double* coarse, double* fine, void*
 int tdg_prolong_add(const tdg_transfer* t, const double* Qc, const double* Qc0, double* fine,
                     void* stream);
 
+/* Element metrics on the device (mesh.py:132-164), invariant
+ * curl form: for nel elements with control nodes ctrl (HOST, (nel, a1, a2,
+ * a3, 3) C order, ctrl_shape = {a1, a2, a3} <= 4) and (n1p, n2p, n3p) = npts
+ * solution nodes per direction, writes the HOST arrays jac (nel, n1p, n2p,
+ * n3p), ja (nel, 3 [i], 3 [xyz], n1p, n2p, n3p), coords (nel, n1p, n2p, n3p,
+ * 3) and sizes (nel, 3).  tables: interpolation L[3][8][4] (ctrl -> nodes),
+ * collocation derivative D[3][64] and weights w[3][8] per direction.
+ * Synchronous (a setup call). */
+int tdg_volume_metrics(int32_t nel, const int32_t* ctrl_shape, const double* ctrl, const int32_t* npts,
+                       const double* tables, double* jac, double* ja, double* coords, double* sizes);
 /* Lifted BR1 gradient (operators.py:224-265; debug/parity): one trace + lift
  * pass over Q (coupled or isolated) that writes the per-node gradient,
  * [3][ngv][n] per element in slot order, to dst (device). */

@@ -53,6 +53,32 @@ def _cross_ja(a1, a2, a3):
     return np.stack([np.cross(a2, a3), np.cross(a3, a1), np.cross(a1, a2)], axis=0)
 
 
+def map_points_ordered(ctrl, xi, eta, zeta):
+    """map_points with a fixed summation order: x = sum over control nodes
+    (a, b, c ascending) of ((l_a l_b) l_c) X_abc, each product and sum
+    separately rounded — the arithmetic of the device metrics kernel
+    (csrc/geometry.cuh), so the curl-form setup is bit-identical on both."""
+    m = [s - 1 for s in ctrl.shape[:3]]
+    l = [spectral.lagrange_values(_ctrl_grid(m[d]), p) for d, p in enumerate((xi, eta, zeta))]
+    out = np.zeros((len(l[0]), len(l[1]), len(l[2]), 3))
+    for a in range(m[0] + 1):
+        for b in range(m[1] + 1):
+            lab = l[0][:, a][:, None] * l[1][:, b][None, :]
+            for c in range(m[2] + 1):
+                lw = lab[:, :, None] * l[2][:, c][None, None, :]
+                out += lw[..., None] * ctrl[a, b, c][None, None, None, :]
+    return out
+
+
+def _d_ordered(arr, axis, D):
+    """Collocation derivative with the kernel's summation order (m ascending)."""
+    a = np.moveaxis(arr, axis, -1)
+    out = np.zeros_like(a)
+    for m in range(a.shape[-1]):
+        out += D[:, m] * a[..., m:m + 1]
+    return np.moveaxis(out, -1, axis)
+
+
 def _d(arr, axis, D):
     """Collocation derivative of a nodal (n1,n2,n3) array along ``axis``."""
     return np.moveaxis(np.einsum("im,...m->...i", D, np.moveaxis(arr, axis, -1)), -1, axis)
@@ -115,10 +141,12 @@ def volume_metrics(ctrl, orders, family="LG", form="cross", index=-1):
         jac = np.einsum("ijkx,ijkx->ijk", a1, np.cross(a2, a3))
         av = (a1, a2, a3)
     elif form == "curl":
-        X = map_points(ctrl, q[0][0], q[1][0], q[2][0])          # (n1,n2,n3,3)
-        X = X - X.reshape(-1, 3).mean(axis=0)                      # element-local origin
+        # fixed summation orders, separately rounded products and sums, node 0
+        # as the local origin: bit-identical to the device kernel
+        X = map_points_ordered(ctrl, q[0][0], q[1][0], q[2][0])  # (n1,n2,n3,3)
+        X = X - X[0, 0, 0]                                         # element-local origin
         D = [spectral.differentiation_matrix(int(n), family) for n in orders]
-        gX = [[_d(X[..., c], k, D[k]) for k in range(3)] for c in range(3)]  # gX[c][k]
+        gX = [[_d_ordered(X[..., c], k, D[k]) for k in range(3)] for c in range(3)]  # gX[c][k]
         ja = np.empty((3, 3) + X.shape[:3])
         for n in range(3):
             mm, ll = (n + 1) % 3, (n + 2) % 3
@@ -126,16 +154,31 @@ def volume_metrics(ctrl, orders, family="LG", form="cross", index=-1):
             V = [X[..., ll] * gX[mm][k] - X[..., mm] * gX[ll][k] for k in range(3)]
             for i in range(3):
                 j, k = (i + 1) % 3, (i + 2) % 3
-                curl_i = _d(V[k], j, D[j]) - _d(V[j], k, D[k])
+                curl_i = _d_ordered(V[k], j, D[j]) - _d_ordered(V[j], k, D[k])
                 ja[i, n] = -0.5 * curl_i
         av = tuple(np.stack([gX[c][k] for c in range(3)], axis=-1) for k in range(3))
-        jac = np.einsum("ijkx,ijkx->ijk", av[0], np.cross(av[1], av[2]))
+        c1 = av[1][..., 1] * av[2][..., 2] - av[1][..., 2] * av[2][..., 1]
+        c2 = av[1][..., 2] * av[2][..., 0] - av[1][..., 0] * av[2][..., 2]
+        c3 = av[1][..., 0] * av[2][..., 1] - av[1][..., 1] * av[2][..., 0]
+        jac = av[0][..., 0] * c1 + av[0][..., 1] * c2 + av[0][..., 2] * c3
         aff, A = affine_map(ctrl[None])
         if aff[0]:
             jc, jac_c = affine_constants(A)
             ja = np.broadcast_to(jac_c[0][:, :, None, None, None], ja.shape).copy()
             jac = np.full(jac.shape, jc[0])
             av = tuple(np.broadcast_to(A[0, d], av[d].shape).copy() for d in range(3))
+        if np.min(jac) <= 0.0:
+            raise MeshError(f"inverted element {index}: min Jacobian {np.min(jac):.3e}")
+        www = (q[0][1][:, None, None] * q[1][1][None, :, None] * q[2][1][None, None, :]).ravel()
+        sizes = np.zeros(3)
+        for d in range(3):
+            nrm = np.sqrt(av[d][..., 0] * av[d][..., 0] + av[d][..., 1] * av[d][..., 1]
+                          + av[d][..., 2] * av[d][..., 2]).ravel()
+            acc = 0.0
+            for t in range(len(www)):            # node order, as the kernel's sum
+                acc += www[t] * nrm[t]
+            sizes[d] = acc / 4.0
+        return jac, ja, sizes
     else:
         raise ValueError(f"unknown metric form {form!r}")
     if np.min(jac) <= 0.0:

@@ -93,7 +93,8 @@ class DGOperator:
                 jac.append(j)
                 ja.append(a)
                 sizes.append(s)
-                coords.append(geometry.map_points(self.mesh.nodes[e], *go.x))
+                coords.append(geometry.map_points_ordered(self.mesh.nodes[e], *go.x) if self.form == "curl"
+                              else geometry.map_points(self.mesh.nodes[e], *go.x))
             go.jac = np.stack(jac)
             go.ja = np.stack(ja)                       # (B, 3, 3, n1, n2, n3)
             go.sizes = np.array(sizes)

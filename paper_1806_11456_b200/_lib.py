@@ -68,6 +68,7 @@ SIGNATURES = {
     "tdg_loop_test": ([_VP, _VP, _VP, _VP, _VP, _dbl, C.c_int, _VP, C.c_int], C.c_int),
     "tdg_loop_end": ([_VP], C.c_int),
     "tdg_stream_create": ([C.POINTER(_VP)], C.c_int),
+    "tdg_volume_metrics": ([_i32, _pi32, _pd, _pi32, _pd, _pd, _pd, _pd, _pd], C.c_int),
     "tdg_stream_destroy": ([_VP], C.c_int),
     "tdg_plan_info": ([_VP, _pi32, _pi32, _pi32], C.c_int),
     "tdg_tau_from_avalue": ([_VP, _VP, _VP, _VP, _VP], C.c_int),

@@ -18,6 +18,7 @@
 #include "../../include/taudg.h"
 #include "common.cuh"
 #include "faces.cuh"
+#include "geometry.cuh"
 #include "laws.cuh"
 #include "transfer.cuh"
 #include "volume.cuh"
@@ -1082,6 +1083,40 @@ int tdg_loop_begin(void* stream, void* body_stream, tdg_loop** out) {
     return fail(TDG_E_CUDA, std::string("tdg_loop_begin: ") + cudaGetErrorString(e));
   }
   *out = lp;
+  return TDG_OK;
+}
+
+int tdg_volume_metrics(int32_t nel, const int32_t* ctrl_shape, const double* ctrl, const int32_t* npts,
+                       const double* tables, double* jac, double* ja, double* coords, double* sizes) {
+  if (!ctrl_shape || !npts || !tables || (nel > 0 && (!ctrl || !jac || !ja || !coords || !sizes)))
+    return fail(TDG_E_ARG, "null argument");
+  if (nel <= 0) return TDG_OK;
+  const int a1 = ctrl_shape[0], a2 = ctrl_shape[1], a3 = ctrl_shape[2];
+  const int n1p = npts[0], n2p = npts[1], n3p = npts[2];
+  if (a1 < 1 || a2 < 1 || a3 < 1 || a1 > 4 || a2 > 4 || a3 > 4)
+    return fail(TDG_E_CONFIG, "device metrics: mapping orders must lie in 0..3");
+  if (n1p < 1 || n2p < 1 || n3p < 1 || n1p > 8 || n2p > 8 || n3p > 8)
+    return fail(TDG_E_CONFIG, "device metrics: solution orders must lie in 0..7");
+  const size_t n = static_cast<size_t>(n1p) * n2p * n3p, ne = static_cast<size_t>(nel);
+  const size_t nc = ne * a1 * a2 * a3 * 3;
+  Allocs mem;
+  double *d_ctrl, *d_jac, *d_ja, *d_x, *d_h;
+  GeoTables* d_tab;
+  int rc = mem.upload(ctrl, nc, &d_ctrl);
+  if (!rc) rc = mem.upload(reinterpret_cast<const GeoTables*>(tables), 1, &d_tab);
+  if (!rc) rc = mem.zeros(ne * n, &d_jac);
+  if (!rc) rc = mem.zeros(ne * n * 9, &d_ja);
+  if (!rc) rc = mem.zeros(ne * n * 3, &d_x);
+  if (!rc) rc = mem.zeros(ne * 3, &d_h);
+  if (rc) return rc;
+  const size_t smem = 15 * n * sizeof(double);
+  if ((rc = allow_smem(k_volume_metrics, smem))) return rc;
+  k_volume_metrics<<<nel, GEO_THREADS, smem>>>(d_ctrl, a1, a2, a3, n1p, n2p, n3p, d_tab, d_jac, d_ja, d_x, d_h);
+  LAUNCH_CHECK("k_volume_metrics");
+  CUDA_TRY(cudaMemcpy(jac, d_jac, ne * n * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(ja, d_ja, ne * n * 9 * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(coords, d_x, ne * n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(sizes, d_h, ne * 3 * sizeof(double), cudaMemcpyDeviceToHost));
   return TDG_OK;
 }
 

@@ -50,6 +50,31 @@ def map_derivs(nodes, xs, ys, zs):
     return out
 
 
+def map_points_ordered(nodes, xs, ys, zs):
+    """map_points with the device kernel's fixed summation order (control nodes
+    a, b, c ascending, ((l_a l_b) l_c) X_abc, separately rounded): the
+    curl-form setup is bit-identical on host, device and oracle."""
+    m = [s - 1 for s in nodes.shape[1:4]]
+    L = [_lag(m[0], xs), _lag(m[1], ys), _lag(m[2], zs)]
+    out = np.zeros((nodes.shape[0], len(L[0]), len(L[1]), len(L[2]), 3))
+    for a in range(m[0] + 1):
+        for b in range(m[1] + 1):
+            lab = L[0][:, a][:, None] * L[1][:, b][None, :]
+            for c in range(m[2] + 1):
+                lw = lab[:, :, None] * L[2][:, c][None, None, :]
+                out += lw[None, ..., None] * nodes[:, a, b, c][:, None, None, None, :]
+    return out
+
+
+def _coll_ordered(arr, axis, D):
+    """Collocation derivative along ``axis`` (1..3) with the kernel's order."""
+    a = np.moveaxis(arr, axis, -1)
+    out = np.zeros_like(a)
+    for m in range(a.shape[-1]):
+        out += D[:, m] * a[..., m:m + 1]
+    return np.moveaxis(out, -1, axis)
+
+
 def _coll(arr, axis, D):
     """Collocation derivative along spatial ``axis`` (1..3) of (B, n1, n2, n3)."""
     return np.moveaxis(np.einsum("im,...m->...i", D, np.moveaxis(arr, axis, -1)), -1, axis)
@@ -94,8 +119,76 @@ def affine_constants(A):
     return jac, ja
 
 
-def volume_metrics(nodes, orders, family, form, ids=None):
-    """Returns J (B,n1,n2,n3), Ja (B,3,3,n1,n2,n3) [i, phys], sizes (B,3), coords."""
+def _device_curl_metrics(nodes, orders, family):
+    """The curl-form J, Ja, sizes and coordinates from the sm_100a kernel
+    (tdg_volume_metrics; same arithmetic as the host branch below up to
+    summation order)."""
+    import ctypes as C
+
+    from . import _lib
+
+    B = nodes.shape[0]
+    a = [int(s) for s in nodes.shape[1:4]]
+    npts = [int(o) + 1 for o in orders]
+    tab = np.zeros(3 * 8 * 4 + 3 * 64 + 3 * 8)
+    L = tab[:96].reshape(3, 8, 4)
+    Dt = tab[96:288].reshape(3, 8, 8)
+    W = tab[288:].reshape(3, 8)
+    for d in range(3):
+        x, w = spectral.rule(int(orders[d]), family)
+        L[d, :npts[d], :a[d]] = _lag(a[d] - 1, x)
+        Dt[d, :npts[d], :npts[d]] = spectral.derivative_matrix(x)
+        W[d, :npts[d]] = w
+    ctrl = np.ascontiguousarray(nodes, dtype=np.float64)
+    n1, n2, n3 = npts
+    jac = np.empty((B, n1, n2, n3))
+    ja = np.empty((B, 3, 3, n1, n2, n3))
+    coords = np.empty((B, n1, n2, n3, 3))
+    sizes = np.empty((B, 3))
+    p = lambda arr, t: arr.ctypes.data_as(C.POINTER(t))
+    sh = np.array(a, np.int32)
+    nn = np.array(npts, np.int32)
+    _lib.call("tdg_volume_metrics", B, p(sh, C.c_int32), p(ctrl, C.c_double), p(nn, C.c_int32),
+              p(tab, C.c_double), p(jac, C.c_double), p(ja, C.c_double), p(coords, C.c_double),
+              p(sizes, C.c_double))
+    return jac, ja, sizes, coords
+
+
+def _jac_ordered(av):
+    """J = a_1 . (a_2 x a_3), separately rounded in a fixed order."""
+    c1 = av[1][..., 1] * av[2][..., 2] - av[1][..., 2] * av[2][..., 1]
+    c2 = av[1][..., 2] * av[2][..., 0] - av[1][..., 0] * av[2][..., 2]
+    c3 = av[1][..., 0] * av[2][..., 1] - av[1][..., 1] * av[2][..., 0]
+    return av[0][..., 0] * c1 + av[0][..., 1] * c2 + av[0][..., 2] * c3
+
+
+def _sizes_ordered(av, w):
+    """h_d = sum_t w_t |a_d(t)| / 4, summed in node order (the kernel's loop)."""
+    www = (w[0][:, None, None] * w[1][None, :, None] * w[2][None, None, :]).ravel()
+    B = av[0].shape[0]
+    out = np.zeros((B, 3))
+    for d in range(3):
+        a = av[d]
+        nrm = np.sqrt(a[..., 0] * a[..., 0] + a[..., 1] * a[..., 1] + a[..., 2] * a[..., 2]).reshape(B, -1)
+        acc = np.zeros(B)
+        for t in range(len(www)):
+            acc += www[t] * nrm[:, t]
+        out[:, d] = acc / 4.0
+    return out
+
+
+def _check_jac(jac, ids):
+    if jac.size and np.min(jac) <= 0.0:
+        bad = int(np.argmin(jac.reshape(len(jac), -1).min(axis=1)))
+        e = bad if ids is None else int(ids[bad])
+        raise MeshError(f"inverted element {e}: min Jacobian {np.min(jac):.3e}")
+
+
+def volume_metrics(nodes, orders, family, form, ids=None, device=None):
+    """Returns J (B,n1,n2,n3), Ja (B,3,3,n1,n2,n3) [i, phys], sizes (B,3), coords.
+
+    ``device="cuda"`` builds the curl form on the GPU (tdg_volume_metrics);
+    the affine override and the Jacobian check stay here."""
     m = [s - 1 for s in nodes.shape[1:4]]
     # cross form: sub/isoparametric only (reference mesh.py:147-152); the
     # invariant curl form uses the interpolant I^N of the map (PAPER.md:144-149)
@@ -104,29 +197,41 @@ def volume_metrics(nodes, orders, family, form, ids=None):
             raise MeshError(f"mapping order {tuple(m)} exceeds solution order {tuple(orders)}")
     x = [spectral.rule(int(n), family)[0] for n in orders]
     w = [spectral.rule(int(n), family)[1] for n in orders]
-    coords = map_points(nodes, *x)
     if form == "cross":
+        coords = map_points(nodes, *x)
         a = map_derivs(nodes, *x)
         ja = np.stack([np.cross(a[1], a[2]), np.cross(a[2], a[0]), np.cross(a[0], a[1])], axis=1)
         ja = np.moveaxis(ja, -1, 2)                       # (B, 3[i], 3[n], ...)
         jac = np.einsum("Eijkx,Eijkx->Eijk", a[0], np.cross(a[1], a[2]))
         av = a
+    elif form == "curl" and device == "cuda" and max(m) <= 3:
+        jac, ja, sizes, coords = _device_curl_metrics(nodes, orders, family)
+        aff, A = affine_map(nodes)
+        if aff.any():
+            jc, jac_c = affine_constants(A[aff])
+            ja[aff] = jac_c[:, :, :, None, None, None]
+            jac[aff] = jc[:, None, None, None]
+            shape = (int(aff.sum()),) + jac.shape[1:] + (3,)
+            sizes[aff] = _sizes_ordered([np.broadcast_to(A[aff][:, d][:, None, None, None, :], shape)
+                                         for d in range(3)], w)
+        _check_jac(jac, ids)
+        return jac, ja, sizes, coords
     elif form == "curl":
+        # same fixed-order arithmetic as the device kernel (tdg_volume_metrics)
+        # and the oracle: bit-identical metrics on all three
         D = [spectral.derivative_matrix(xx) for xx in x]
-        # element-local origin: the curl form is translation invariant (the
-        # tensor-product derivatives commute), and local coordinates avoid
-        # multiplying O(1) positions into an O(h^2) result
-        X = coords - coords.reshape(len(coords), -1, 3).mean(axis=1)[:, None, None, None, :]
-        g = [[_coll(X[..., c], k + 1, D[k]) for k in range(3)] for c in range(3)]
+        coords = map_points_ordered(nodes, *x)
+        X = coords - coords[:, :1, :1, :1, :]                 # element-local origin: node 0
+        g = [[_coll_ordered(X[..., c], k + 1, D[k]) for k in range(3)] for c in range(3)]
         ja = np.empty((X.shape[0], 3, 3) + X.shape[1:4])
         for n in range(3):
             mm, ll = (n + 1) % 3, (n + 2) % 3
             V = [X[..., ll] * g[mm][k] - X[..., mm] * g[ll][k] for k in range(3)]
             for i in range(3):
                 j, k = (i + 1) % 3, (i + 2) % 3
-                ja[:, i, n] = -0.5 * (_coll(V[k], j + 1, D[j]) - _coll(V[j], k + 1, D[k]))
+                ja[:, i, n] = -0.5 * (_coll_ordered(V[k], j + 1, D[j]) - _coll_ordered(V[j], k + 1, D[k]))
         av = [np.stack([g[c][k] for c in range(3)], axis=-1) for k in range(3)]
-        jac = np.einsum("Eijkx,Eijkx->Eijk", av[0], np.cross(av[1], av[2]))
+        jac = _jac_ordered(av)
         aff, A = affine_map(nodes)
         if aff.any():
             jc, jac_c = affine_constants(A[aff])
@@ -134,6 +239,8 @@ def volume_metrics(nodes, orders, family, form, ids=None):
             jac[aff] = jc[:, None, None, None]
             for d in range(3):
                 av[d][aff] = A[aff][:, d][:, None, None, None, :]
+        _check_jac(jac, ids)
+        return jac, ja, _sizes_ordered(av, w), coords
     else:
         raise ValueError(f"unknown metric form {form!r}")
     if jac.size and np.min(jac) <= 0.0:

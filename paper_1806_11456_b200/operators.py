@@ -92,7 +92,7 @@ class DGOperator:
         for g, (sig, ids) in enumerate(zip(of.group_orders, of.group_elements)):
             s0 = of.group_slot0[g]
             nodes = msh.nodes[ids]
-            jac, ja, sz, coords = geometry.volume_metrics(nodes, sig, fam, self.form, ids)
+            jac, ja, sz, coords = geometry.volume_metrics(nodes, sig, fam, self.form, ids, device=self.device)
             self._coords.append(coords)
             self._jac.append(jac)
             self._vol_ja.append(ja)
@@ -185,16 +185,29 @@ class DGOperator:
         idx_int = np.flatnonzero(interior)
         info = np.zeros((len(idx_int), 12), np.int32)
         mortar_keys = {}
-        for k, f in enumerate(idx_int):
-            el, sl, er, sr, o = int(L[f]), int(SL[f]), int(R[f]), int(SR[f]), int(O[f])
-            l1, l2 = self._tan(el, sl)
-            r1, r2 = self._tan(er, sr)
-            if o & 4:
-                r1, r2 = r2, r1
-            m1, m2 = max(l1, r1), max(l2, r2)
-            info[k] = (of.slot_of_elem[el], sl, of.slot_of_elem[er], sr, o, l1, l2, r1, r2, m1, m2, 0)
-            g = int(of.element_slot[el, 0])
-            mortar_keys.setdefault((g, sl, m1, m2), []).append(k)
+        if len(idx_int):
+            # tangential orders of both sides (the right side re-aligned by the
+            # orientation's swap bit) and the mortar orders, for all faces at once
+            ta = np.array([geometry.face_dirs(s)[1] for s in range(6)])
+            tb = np.array([geometry.face_dirs(s)[2] for s in range(6)])
+            el, sl, er, sr, o = L[idx_int], SL[idx_int], R[idx_int], SR[idx_int], O[idx_int]
+            oo = of.orders
+            l1, l2 = oo[el, ta[sl]], oo[el, tb[sl]]
+            r1, r2 = oo[er, ta[sr]], oo[er, tb[sr]]
+            sw = (o & 4) != 0
+            r1, r2 = np.where(sw, r2, r1), np.where(sw, r1, r2)
+            m1, m2 = np.maximum(l1, r1), np.maximum(l2, r2)
+            info[:] = np.stack([of.slot_of_elem[el], sl, of.slot_of_elem[er], sr, o, l1, l2, r1, r2, m1, m2,
+                                np.zeros_like(o)], axis=1)
+            # faces grouped by (left bucket, left side, mortar orders), groups in
+            # order of first appearance, faces ascending inside a group
+            keys = np.stack([of.element_slot[el, 0], sl, m1, m2], axis=1)
+            uk, first, inv = np.unique(keys, axis=0, return_index=True, return_inverse=True)
+            order = np.argsort(first, kind="stable")
+            members = np.argsort(inv.ravel(), kind="stable")
+            bounds = np.concatenate([[0], np.cumsum(np.bincount(inv.ravel(), minlength=len(uk)))])
+            for u in order:
+                mortar_keys[tuple(int(x) for x in uk[u])] = members[bounds[u]:bounds[u + 1]].tolist()
         geo_off = np.zeros(len(idx_int), np.int64)
         geo_chunks = []
         for (g, sl, m1, m2), ks in mortar_keys.items():
