@@ -255,7 +255,8 @@ int setup_attrs(tdg_plan* p) {
   // The limit is a per-function, process-wide attribute shared by every
   // plan: set it to the MAXN-item bound, never to this plan's (smaller) need.
   const size_t ngv = p->ngv, ng = 3 * ngv, nv = p->nv, b = MAXN * sizeof(double);
-  const size_t lift = std::max(ngv + 9, ng) * b, own = (ngv + 9) * b, flux = 3 * nv * b;
+  const size_t lift = std::max(ngv + 9, ng) * b, own = (ngv + std::max<size_t>(9, nv)) * b + 16,
+               flux = 3 * nv * b;
   int rc = with_nx<LAW>(p->iso, [&](auto nx) -> int {
     constexpr int NX = decltype(nx)::value;
     int r;
@@ -770,7 +771,12 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   {
     bool curved = false;
     for (int s = 0; s < ns && !curved; ++s) curved = desc->affine[s] == 0;
-    p->smem_lift_own = static_cast<size_t>(p->ngv + (curved ? 9 : 0)) * mt * sizeof(double);
+    // every item affine: the own-order lift receives the item's Q span by one
+    // TMA bulk copy into the region the curved metrics would use (TDG_TMA_Q=0: LDG)
+    const char* tq = getenv("TDG_TMA_Q");
+    d.tma_q = (!curved && !(tq && tq[0] == '0')) ? 1 : 0;
+    p->smem_lift_own = static_cast<size_t>(p->ngv + (curved ? 9 : 0)) * mt * sizeof(double) +
+                       (d.tma_q ? (static_cast<size_t>(p->nv) * mt + 2) * sizeof(double) : 0);
   }
   p->smem_flux = static_cast<size_t>(3 * p->nv) * mt * sizeof(double);
   if (p->viscous) {

@@ -55,6 +55,8 @@ struct DevPlan {
   int nsm;        // SMs: kernels prefetch the work about one wave ahead (L2)
   int pf_trace, pf_face, pf_down;   // look-ahead distances, blocks per SM
   int pf_item;    // element kernels: L2 bulk prefetch of the item's own spans
+  int tma_q;      // lift (own-order plans, every item affine): the item's Q span
+                  // arrives in shared memory by one TMA bulk copy
   int collapsed;  // bit d: direction d has order 0 on every element (2D extrusion)
   // side work items for side kernels: (slot, side | kind<<8), ghost offset
   int nside_iso;
@@ -222,6 +224,62 @@ __device__ __forceinline__ void side_dirs(int side, int& d, int& a, int& b) {
   d = side >> 1;
   a = (d == 0) ? 1 : 0;
   b = (d == 2) ? 1 : 2;
+}
+
+}  // namespace tdg
+
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk) completing on an mbarrier
+namespace tdg {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Copy doubles [src, src+count) into shared memory at a 16-byte aligned
+// ``dst`` with one bulk copy; returns the index offset (0 or 1) at which the
+// data starts in ``dst`` (the source span is widened to 16-byte boundaries,
+// so buffers need >= 8 bytes of slack past their end).
+__device__ __forceinline__ int bulk_span(double* dst, const double* src, long long count,
+                                         unsigned long long* bar, uint32_t& bytes_total) {
+  const unsigned long long a = reinterpret_cast<unsigned long long>(src);
+  const unsigned long long lo = a & ~15ull;
+  const unsigned long long hi = (a + 8ull * count + 15ull) & ~15ull;
+  const uint32_t bytes = static_cast<uint32_t>(hi - lo);
+  bulk_g2s(dst, reinterpret_cast<const void*>(lo), bytes, bar);
+  bytes_total += bytes;
+  return static_cast<int>((a - lo) >> 3);
 }
 
 }  // namespace tdg

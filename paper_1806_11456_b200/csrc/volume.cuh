@@ -514,16 +514,52 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
   double qa[NPT][NV];
-  load_item_state<NV>(P, Q, wi, n, tot, qa);
-  if (coupled && P.gstar)
-    prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
-  else
-    prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
-  if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
-  load_tables(P, N1, N2, N3, T);
-  const bool aff = P.work_aff[blockIdx.x] != 0;
+  __shared__ unsigned long long qbar;
   double* gs = sm;               // [NGV][tot]
   double* js = sm + NGV * tot;   // [9][tot]  (curved items only)
+  const bool tma = P.tma_q != 0;
+  if (tma) {
+    // the item's slots are contiguous in Q: one bulk copy of [nv][n] x E
+    // (16-byte aligned span; data starts `shift` doubles in) into shared
+    // memory after the g region, while the tables are staged
+    double* qs = sm + ((NGV * tot + 1) & ~1);   // 16-byte aligned destination
+    const long long n0 = P.node_off[wi.x];
+    const double* src = Q + n0 * NV;
+    const int shift = static_cast<int>((reinterpret_cast<unsigned long long>(src) & 15ull) >> 3);
+    if (threadIdx.x == 0) {
+      mbar_init(&qbar, 1);
+      mbar_fence_init();
+      const unsigned long long a = reinterpret_cast<unsigned long long>(src);
+      const unsigned long long lo = a & ~15ull, hi = (a + 8ull * NV * tot + 15ull) & ~15ull;
+      mbar_expect_tx(&qbar, static_cast<uint32_t>(hi - lo));
+      bulk_g2s(qs, reinterpret_cast<const void*>(lo), static_cast<uint32_t>(hi - lo), &qbar);
+    }
+    if (coupled && P.gstar)
+      prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
+    else
+      prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+    load_tables(P, N1, N2, N3, T);
+    __syncthreads();   // mbarrier initialised before anyone waits on it
+    mbar_wait(&qbar, 0);
+#pragma unroll
+    for (int r = 0; r < NPT; ++r) {
+      const int t = threadIdx.x + r * blockDim.x;
+      if (t < tot) {
+        const int e = t / n, node = t - e * n;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) qa[r][v] = qs[shift + (e * NV + v) * n + node];
+      }
+    }
+  } else {
+    load_item_state<NV>(P, Q, wi, n, tot, qa);
+    if (coupled && P.gstar)
+      prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
+    else
+      prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+    if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
+    load_tables(P, N1, N2, N3, T);
+  }
+  const bool aff = P.work_aff[blockIdx.x] != 0;
   // staging needs no table: one barrier covers both
   stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
   __syncthreads();
