@@ -31,7 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r02", "ncu_summary.json")
 # the unmodified reference (pure Python, not present on the GPU box) timed in the
 # build container on its own 2D-scalar analogues of configs 1-2
 REF2D = os.path.join(ROOT, "profiles", "reference_cpu_2d.json")

@@ -89,7 +89,8 @@ def launches(path):
 
 if __name__ == "__main__":
     c3, c4, ll, out, src = sys.argv[1:6]
-    res = {"round": 1, "source": src, "kernels": raw(c3), "cfg4_kernels": raw(c4),
+    rnd = int(sys.argv[6]) if len(sys.argv) > 6 else 1
+    res = {"round": rnd, "source": src, "kernels": raw(c3), "cfg4_kernels": raw(c4),
            "launch_list_ns_by_kernel": launches(ll)}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps({k: v["dram_bytes_per_launch"] for k, v in res["kernels"].items()}))
