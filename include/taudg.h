@@ -222,8 +222,9 @@ int tdg_gradient(tdg_plan* plan, const double* Q, int isolated, double* dst, voi
  * element-kernel launch), conforming and nonconforming (mortar) interior faces. */
 int tdg_plan_info(const tdg_plan* plan, int32_t* nwork, int32_t* nconf_faces, int32_t* nmortar_faces);
 /* Debug/parity: copy a face scratch buffer of the last evaluation to dst
- * (device): which = 0 Q traces [nv], 1 lift surface [3 ngv], 2 gradient
- * traces [3 ngv], 3 flux surface [nv]; per element side at side_off*C as
+ * (device): which = 0 Q traces [nv], 1 lift surface [3 ngv], 2 viscous
+ * traces (scalar laws: gradient [3 ngv]; Navier-Stokes: the side's own
+ * F_v.n sigma [4]), 3 flux surface [nv]; per element side at side_off*C as
  * [C][nf] with t1 fastest.  Returns the element count in *len_out. */
 int tdg_debug_copy(tdg_plan* plan, int which, double* dst, int64_t* len_out, void* stream);
 

@@ -11,7 +11,10 @@
                                                                (:224-265)
 * face fluxes: Riemann + mean viscous flux on interior mortars, Riemann with
   the ghost + interior viscous flux on boundaries, and the analytic own-trace
-  flux for every side in the isolated variant                  (:292-334)
+  flux for every side in the isolated variant                  (:292-334).
+  Scalar laws take the gradient traces to the mortar as the reference does;
+  Navier-Stokes (no reference counterpart) takes each side's own normal
+  viscous flux F_v(q, G).n sigma there (``law.side_flux_traces``)
 * A = F / M, r = S - A, tau_e = max |M (S_pde - A)|            (:337-364)
 
 Differences from the reference, all recorded in DESIGN.md: 3D, nv unknowns,
@@ -316,6 +319,17 @@ class DGOperator:
         def normal_flux(fl, n):
             return np.einsum("bd...,bdv...->bv...", n, fl)
 
+        side_fv = visc and getattr(law, "side_flux_traces", False)
+        if side_fv:
+            # traces of the lifted variables: every side's own F_v.n sigma at
+            # its own face nodes comes from them and the gradient traces
+            trv = self._traces([law.grad_vars(b) for b in Q.blocks])
+
+            def side_fv_sigma(g, s, rows, kind=None):
+                go = self.group_ops[g]
+                return (law.side_visc_normal(trv[g][s][rows], trg[g][s][rows], go.side_normal[s][rows], kind)
+                        * go.side_sigma[s][rows][:, None])
+
         if isolated:
             for g, go in enumerate(self.group_ops):
                 rows = np.arange(Q.blocks[g].shape[0])
@@ -323,6 +337,10 @@ class DGOperator:
                     q_in = trq[g][s]
                     n = go.side_normal[s]
                     flux = normal_flux(law.adv_flux(q_in), n)
+                    if side_fv:
+                        self._scatter(out.blocks, g, rows, s,
+                                      flux * go.side_sigma[s][:, None] - side_fv_sigma(g, s, rows))
+                        continue
                     if visc:
                         flux = flux - normal_flux(law.visc_flux(q_in, trg[g][s]), n)
                     self._scatter(out.blocks, g, rows, s, flux * go.side_sigma[s][:, None])
@@ -331,6 +349,10 @@ class DGOperator:
             q_in = trq[fg.g][fg.s][fg.rows]
             qg = law.bc_riemann_ghost(q_in, fg.normal, fg.kind, fg.ghost)
             flux = law.riemann(q_in, qg, fg.normal)
+            if side_fv:
+                self._scatter(out.blocks, fg.g, fg.rows, fg.s,
+                              flux * fg.sigma[:, None] - side_fv_sigma(fg.g, fg.s, fg.rows, fg.kind))
+                continue
             if visc:
                 flux = flux - law.bc_visc_normal(q_in, trg[fg.g][fg.s][fg.rows], fg.normal, fg.kind)
             self._scatter(out.blocks, fg.g, fg.rows, fg.s, flux * fg.sigma[:, None])
@@ -340,13 +362,20 @@ class DGOperator:
             qlm = self._up(fg.upL, ql)
             qrm = self._up(fg.upR, qr)
             flux = law.riemann(qlm, qrm, fg.normal)
-            if visc:
-                gl = self._up(fg.upL, trg[fg.gl][fg.sl][fg.rows_l])
-                gr = self._up(fg.upR, _aligned_from_right(trg[fg.gr][fg.sr][fg.rows_r], fg.orient))
-                fv = 0.5 * (normal_flux(law.visc_flux(qlm, gl), fg.normal)
-                            + normal_flux(law.visc_flux(qrm, gr), fg.normal))
-                flux = flux - fv
-            val = flux * fg.sigma[:, None]
+            if side_fv:
+                # mortar mean of the two sides' interpolated normal viscous
+                # fluxes; the right side's carries its own (opposite) normal
+                fl = self._up(fg.upL, side_fv_sigma(fg.gl, fg.sl, fg.rows_l))
+                fr = self._up(fg.upR, _aligned_from_right(side_fv_sigma(fg.gr, fg.sr, fg.rows_r), fg.orient))
+                val = flux * fg.sigma[:, None] - 0.5 * (fl - fr)
+            else:
+                if visc:
+                    gl = self._up(fg.upL, trg[fg.gl][fg.sl][fg.rows_l])
+                    gr = self._up(fg.upR, _aligned_from_right(trg[fg.gr][fg.sr][fg.rows_r], fg.orient))
+                    fv = 0.5 * (normal_flux(law.visc_flux(qlm, gl), fg.normal)
+                                + normal_flux(law.visc_flux(qrm, gr), fg.normal))
+                    flux = flux - fv
+                val = flux * fg.sigma[:, None]
             self._scatter(out.blocks, fg.gl, fg.rows_l, fg.sl, self._up(fg.dnL, val))
             back = _right_from_aligned(self._up(fg.dnR, val), fg.orient)
             self._scatter(out.blocks, fg.gr, fg.rows_r, fg.sr, -back)

@@ -22,6 +22,9 @@ import numpy as np
 class ScalarLaw:
     nv = 1
     ngv = 1
+    # interior faces carry the gradient traces to the mortar and evaluate the
+    # viscous flux there, as the reference does (operators.py:318-329)
+    side_flux_traces = False
 
     def __init__(self, mu=0.0):
         if mu < 0.0:
@@ -106,6 +109,14 @@ class ViscousBurgers(ScalarLaw):
 class NavierStokes:
     """Compressible NS, q = (rho, rho u, rho v, rho w, rho E)."""
 
+    # Every element side evaluates its own normal viscous flux F_v.n sigma at
+    # its own face nodes — from the traces of the lifted variables (u, v, w, T)
+    # and of their gradient, with the side's own outward normal (boundary
+    # treatment included) — and interior faces average the two sides'
+    # interpolants on the mortar (DESIGN.md §3, decision 3).  The reference has
+    # no Navier-Stokes law; this choice is this repo's.
+    side_flux_traces = True
+
     nv = 5
     ngv = 4
 
@@ -170,12 +181,15 @@ class NavierStokes:
     def visc_flux(self, q, G):
         """(1/Re) [0, tau_dx, tau_dy, tau_dz, u.tau_d + T_d/((g-1) Pr M^2)]."""
         rho, u, v, w, p = self._prim(q)
-        vel = (u, v, w)
+        return self.visc_flux_vel((u, v, w), G)
+
+    def visc_flux_vel(self, vel, G):
+        """The viscous flux from the velocity (u, v, w) and the gradient G."""
         inv_re = 1.0 / self.reynolds
         kappa = 1.0 / ((self.gamma - 1.0) * self.prandtl * self.mach ** 2)
         # G[:, d, k]: d/dx_d of (u, v, w, T)[k]
         div = G[:, 0, 0] + G[:, 1, 1] + G[:, 2, 2]
-        out = np.zeros((q.shape[0], 3, 5) + q.shape[2:])
+        out = np.zeros((G.shape[0], 3, 5) + G.shape[3:])
         for d in range(3):
             tau = []
             for i in range(3):
@@ -189,6 +203,21 @@ class NavierStokes:
             out[:, d, 4] = inv_re * (vel[0] * tau[0] + vel[1] * tau[1] + vel[2] * tau[2]
                                      + kappa * G[:, d, 3])
         return out
+
+    def side_visc_normal(self, gv, G, n, kind=None):
+        """F_v.n at a side's own face nodes from the traces gv (B, ngv, ...) of
+        (u, v, w, T) and G of their gradient; ``kind`` applies the boundary
+        treatment of bc_visc_normal (wall: no slip, adiabatic; symmetry: 0)."""
+        if kind == "symmetry":
+            return np.zeros((gv.shape[0], 5) + gv.shape[2:])
+        if kind == "wall":
+            zero = np.zeros_like(gv[:, 0])
+            Gw = G.copy()
+            Gw[:, :, 3] = 0.0
+            fv = self.visc_flux_vel((zero, zero, zero), Gw)
+        else:
+            fv = self.visc_flux_vel((gv[:, 0], gv[:, 1], gv[:, 2]), G)
+        return np.einsum("bd...,bdv...->bv...", n, fv)
 
     def wave_speed(self, q):
         rho, u, v, w, p = self._prim(q)

@@ -76,6 +76,9 @@ struct Allocs {
 
 int law_nv(int law) { return law == TDG_LAW_NS ? 5 : 1; }
 int law_ngv(int law) { return law == TDG_LAW_NS ? 4 : 1; }
+// components of the viscous side traces (Law::NTR): the gradient for scalar
+// laws, the side's own normal viscous flux for Navier-Stokes
+int law_ntr(int law) { return law == TDG_LAW_NS ? 4 : 3; }
 
 // ---- launch timing -------------------------------------------------------
 struct TimedLaunch {
@@ -151,7 +154,7 @@ __global__ void k_fill(double* p, double v, int n) {
 struct tdg_plan {
   DevPlan d{};
   Allocs mem;
-  int nv = 1, ngv = 1;
+  int nv = 1, ngv = 1, ntr = 3;
   bool viscous = false;
   int64_t nodes = 0;
   std::vector<int> orders_h;      // per slot
@@ -255,7 +258,7 @@ int setup_attrs(tdg_plan* p) {
   // The limit is a per-function, process-wide attribute shared by every
   // plan: set it to the MAXN-item bound, never to this plan's (smaller) need.
   const size_t ngv = p->ngv, ng = 3 * ngv, nv = p->nv, b = MAXN * sizeof(double);
-  const size_t lift = std::max(ngv + 9, ng) * b, own = (ngv + std::max<size_t>(9, nv)) * b + 16,
+  const size_t lift = (LAW == LAW_NS ? ngv + std::max<size_t>(9, ng) : std::max(ngv + 9, ng)) * b, own = (ngv + std::max<size_t>(9, nv)) * b + 16,
                flux = 3 * nv * b;
   int rc = with_nx<LAW>(p->iso, [&](auto nx) -> int {
     constexpr int NX = decltype(nx)::value;
@@ -490,6 +493,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   auto* p = new tdg_plan();
   p->nv = law_nv(desc->law);
   p->ngv = law_ngv(desc->law);
+  p->ntr = law_ntr(desc->law);
   p->viscous = desc->params[3] > 0.0;
   const int ns = desc->nslots;
   p->orders_h.assign(desc->orders, desc->orders + 3 * ns);
@@ -677,6 +681,23 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     const long long go = desc->ghost_off[f];
     bnd.push_back(make_int4(b[0], b[1], b[2], static_cast<int>(go)));
   }
+  // per-side flags: boundary kind + 1 (bits 0-3), uniform own-order geometry (bit 4)
+  std::vector<int> sflags(6 * static_cast<size_t>(ns), 0);
+  for (int f = 0; f < desc->nbfaces; ++f) {
+    const int* b = desc->bface_info + 4 * f;
+    sflags[6 * static_cast<size_t>(b[0]) + b[1]] |= (b[2] + 1) & 15;
+  }
+  for (int s = 0; s < ns; ++s)
+    for (int side = 0; side < 6; ++side) {
+      const int dn = side >> 1, ta = dn == 0 ? 1 : 0, tb = dn == 2 ? 1 : 2;
+      const int nf = (p->orders_h[3 * s + ta] + 1) * (p->orders_h[3 * s + tb] + 1);
+      const double* gg = desc->side_geo + 4 * desc->side_off[6 * s + side];
+      bool uni = true;
+      for (int c = 0; c < 4 && uni; ++c)
+        for (int k = 1; k < nf && uni; ++k) uni = gg[c * nf + k] == gg[c * nf];
+      if (uni) sflags[6 * static_cast<size_t>(s) + side] |= 16;
+    }
+  int* sflags_d = nullptr;
   std::vector<int> work_aff(work.size());
   for (size_t k = 0; k < work.size(); ++k) {
     int a = 1;
@@ -692,6 +713,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   int4 *iso_d, *bnd_d;
   rc = p->mem.upload(work.data(), work.size(), &work_d);
   if (!rc) rc = p->mem.upload(work_aff.data(), work_aff.size(), &work_aff_d);
+  if (!rc && ns > 0) rc = p->mem.upload(sflags.data(), sflags.size(), &sflags_d);
   if (!rc) rc = p->mem.upload(work_ord.data(), work_ord.size(), &work_ord_d);
   if (!rc) rc = p->mem.upload(iso.data(), iso.size(), &iso_d);
   if (!rc) rc = p->mem.upload(bnd.data(), bnd.size(), &bnd_d);
@@ -707,8 +729,8 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   if (!rc) rc = p->mem.zeros(sn * p->nv, &fsurf);
   if (p->viscous) {
     if (!rc) rc = p->mem.zeros(sn * NG, &lsurf);
-    if (!rc) rc = p->mem.zeros(sn * NG, &gtr);
-    if (!rc) rc = p->mem.zeros(tn * NG, &gtrm);
+    if (!rc) rc = p->mem.zeros(sn * p->ntr, &gtr);
+    if (!rc) rc = p->mem.zeros(tn * p->ntr, &gtrm);
     if (!rc) rc = p->mem.zeros(sn * p->ngv, &gsf);
   }
   if (rc) {
@@ -752,6 +774,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   }
   d.work = work_d;
   d.work_aff = work_aff_d;
+  d.side_flags = sflags_d;
   d.work_ord = work_ord_d;
   d.nside_iso = static_cast<int>(iso.size());
   d.side_iso = iso_d;
@@ -767,7 +790,9 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.gsf = gsf;
   // dynamic shared memory sized by the largest work item (<= MAXN nodes)
   const size_t mt = static_cast<size_t>(p->max_tot);
-  p->smem_lift = static_cast<size_t>(std::max(p->ngv + 9, NG)) * mt * sizeof(double);
+  // (Navier-Stokes keeps the lifted variables beside G for the side traces)
+  p->smem_lift = static_cast<size_t>(desc->law == TDG_LAW_NS ? p->ngv + std::max(9, NG)
+                                                             : std::max(p->ngv + 9, NG)) * mt * sizeof(double);
   {
     bool curved = false;
     for (int s = 0; s < ns && !curved; ++s) curved = desc->affine[s] == 0;
@@ -1047,7 +1072,7 @@ int tdg_debug_copy(tdg_plan* p, int which, double* dst, int64_t* len_out, void* 
   switch (which) {
     case 0: src = p->d.qtr; comps = p->nv; break;
     case 1: src = p->d.lsurf; comps = NG; break;
-    case 2: src = p->d.gtr; comps = NG; break;
+    case 2: src = p->d.gtr; comps = p->ntr; break;
     case 3: src = p->d.fsurf; comps = p->nv; break;
     default: return fail(TDG_E_ARG, "unknown buffer");
   }

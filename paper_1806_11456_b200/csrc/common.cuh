@@ -81,10 +81,16 @@ struct DevPlan {
   const int* mface;              // nonconforming interior faces (k_mortar)
   // scratch (device)
   double* qtrm;   // mortar-order Q traces of nonconforming sides (own frame)
-  double* gtrm;   // mortar-order gradient traces of nonconforming sides
+  double* gtrm;   // mortar-order viscous traces of nonconforming sides ([ntr] per node)
   double* qtr;    // [side_nodes][nv] own-order Q traces
   double* lsurf;  // [side_nodes][3*ngv]   lift surface contributions
-  double* gtr;    // [side_nodes][3*ngv] own-order gradient traces
+  // [side_nodes][ntr] own-order viscous traces: the gradient (scalar laws,
+  // ntr = 3 ngv) or the side's own normal viscous flux F_v.n sigma with its
+  // boundary treatment applied (Navier-Stokes, ntr = 4; Law::FVTR)
+  double* gtr;
+  // per element side (slot*6+side): bits 0-3 = boundary kind + 1 (0: interior
+  // side), bit 4 = uniform own-order side geometry (node 0's values serve)
+  const int* side_flags;
   double* fsurf;  // [side_nodes][nv]      flux surface contributions
   double* grad;   // [nodes][3*ngv] lifted gradient
   // conforming-face lift in g* form (LGL plans without nonconforming faces):

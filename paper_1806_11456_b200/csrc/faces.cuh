@@ -40,7 +40,7 @@ __device__ __forceinline__ void face_point(const DevPlan& P, const double* qsrc,
                                            double* val /* [FLUX ? NV : 3 NGV] */,
                                            bool gconst = false) {
   using L = Law<LAW>;
-  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
+  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV, NTR = L::NTR;
   const int tg = gconst ? 0 : t;   // uniform face geometry: node 0's values
   const double sigma = geo[tg];
   const double nrm[3] = {geo[nm + tg], geo[2 * nm + tg], geo[3 * nm + tg]};
@@ -61,6 +61,21 @@ __device__ __forceinline__ void face_point(const DevPlan& P, const double* qsrc,
   } else {
     double F[NV];
     L::riemann(P.prm, ql, qr, nrm, F);
+    if constexpr (L::FVTR) {
+      // each side's own F_v.n sigma (own outward normal), interpolated to this
+      // node: flux sigma - 1/2 (f_L - f_R)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) val[v] = F[v] * sigma;
+      if (L::viscous(P.prm)) {
+#pragma unroll
+        for (int k = 0; k < NTR; ++k) {
+          const double fl = gsrc[tL * NTR + (long long)k * nm + t];
+          const double fr = gsrc[tR * NTR + (long long)k * nm + kR];
+          val[NV - NTR + k] -= 0.5 * (fl - fr);
+        }
+      }
+      return;
+    }
     if (L::viscous(P.prm)) {
       double GL[3][NGV], GR[3][NGV], fl[NV], fr[NV];
 #pragma unroll
@@ -102,8 +117,8 @@ __global__ void __launch_bounds__(FACE_THREADS_MAX) k_face(DevPlan P) {
       l2_prefetch_span(P.qtr + (long long)fn.y * NV, sizeof(double) * mn * NV);
       if (!((fn.z >> 10) & 1)) l2_prefetch_span(P.face_geo + fn.w, sizeof(double) * mn * 4);
       if (FLUX && L::viscous(P.prm)) {
-        l2_prefetch_span(P.gtr + (long long)fn.x * NG, sizeof(double) * mn * NG);
-        l2_prefetch_span(P.gtr + (long long)fn.y * NG, sizeof(double) * mn * NG);
+        l2_prefetch_span(P.gtr + (long long)fn.x * L::NTR, sizeof(double) * mn * L::NTR);
+        l2_prefetch_span(P.gtr + (long long)fn.y * L::NTR, sizeof(double) * mn * L::NTR);
       }
     }
   }
@@ -209,8 +224,8 @@ __global__ void __launch_bounds__(32 * MORTAR_WARPS, (FLUX ? 4 : 5) * 4 / MORTAR
       l2_prefetch_span(P.qtrm + (long long)fn.y * NV, sizeof(double) * mn * NV);
       l2_prefetch_span(P.face_geo + fn.w, sizeof(double) * mn * 4);
       if (FLUX && L::viscous(P.prm)) {
-        l2_prefetch_span(P.gtrm + (long long)fn.x * NG, sizeof(double) * mn * NG);
-        l2_prefetch_span(P.gtrm + (long long)fn.y * NG, sizeof(double) * mn * NG);
+        l2_prefetch_span(P.gtrm + (long long)fn.x * L::NTR, sizeof(double) * mn * L::NTR);
+        l2_prefetch_span(P.gtrm + (long long)fn.y * L::NTR, sizeof(double) * mn * L::NTR);
       }
     }
   }
@@ -266,6 +281,29 @@ __global__ void __launch_bounds__(SIDE_THREADS) k_side(DevPlan P, const int4* __
   } else {
     const bool visc = L::viscous(P.prm);
     double F[NV];
+    if constexpr (L::FVTR) {
+      // the lift kernel left this side's F_v.n sigma (boundary treatment
+      // applied) in the own-order viscous traces
+      if (kind < 0) {
+        double f[3][NV];
+        L::adv_flux(P.prm, q, f);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) F[v] = f[0][v] * nrm[0] + f[1][v] * nrm[1] + f[2][v] * nrm[2];
+      } else {
+        double qg[NV];
+        L::bc_ghost(P.prm, q, nrm, kind, gh, qg);
+        L::riemann(P.prm, q, qg, nrm, F);
+      }
+      double* dst = P.fsurf + so * NV + kf;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        double x = F[v] * sigma;
+        if (visc && v >= NV - L::NTR)
+          x -= P.gtr[to * L::NTR + (long long)(v - (NV - L::NTR)) * nf + kf];
+        dst[(long long)v * nf] = x;
+      }
+      return;
+    }
     double G[3][NGV];
     if (visc) {
 #pragma unroll

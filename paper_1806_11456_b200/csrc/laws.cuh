@@ -21,6 +21,10 @@ struct Law;
 template <>
 struct Law<LAW_ADVDIFF> {
   static constexpr int NV = 1, NGV = 1;
+  // side traces of the viscous term: the gradient itself, taken to the mortar
+  // as the reference does (operators.py:318-329)
+  static constexpr bool FVTR = false;
+  static constexpr int NTR = 3 * NGV;
   __device__ static bool viscous(const double* P) { return P[3] > 0.0; }
   __device__ static void grad_vars(const double*, const double* q, double* g) { g[0] = q[0]; }
   __device__ static void adv_flux(const double* P, const double* q, double f[3][NV]) {
@@ -39,6 +43,8 @@ struct Law<LAW_ADVDIFF> {
                                      const double* n, double* out) {
     out[0] = P[3] * (G[0][0] * n[0] + G[1][0] * n[1] + G[2][0] * n[2]);
   }
+  __device__ static void side_visc(const double*, const double*, const double[3][NGV], const double*,
+                                   double, int, double*) {}
   __device__ static double wave_speed(const double* P, const double*) {
     return sqrt(P[0] * P[0] + P[1] * P[1] + P[2] * P[2]);
   }
@@ -61,6 +67,10 @@ struct Law<LAW_ADVDIFF> {
 template <>
 struct Law<LAW_BURGERS> {
   static constexpr int NV = 1, NGV = 1;
+  // side traces of the viscous term: the gradient itself, taken to the mortar
+  // as the reference does (operators.py:318-329)
+  static constexpr bool FVTR = false;
+  static constexpr int NTR = 3 * NGV;
   __device__ static bool viscous(const double* P) { return P[3] > 0.0; }
   __device__ static void grad_vars(const double*, const double* q, double* g) { g[0] = q[0]; }
   __device__ static void adv_flux(const double* P, const double* q, double f[3][NV]) {
@@ -79,6 +89,8 @@ struct Law<LAW_BURGERS> {
                                      const double* n, double* out) {
     out[0] = P[3] * (G[0][0] * n[0] + G[1][0] * n[1] + G[2][0] * n[2]);
   }
+  __device__ static void side_visc(const double*, const double*, const double[3][NGV], const double*,
+                                   double, int, double*) {}
   __device__ static double wave_speed(const double* P, const double* q) {
     return sqrt(P[0] * P[0] + P[1] * P[1] + P[2] * P[2]) * fabs(q[0]);
   }
@@ -103,6 +115,12 @@ struct Law<LAW_BURGERS> {
 template <>
 struct Law<LAW_NS> {
   static constexpr int NV = 5, NGV = 4;
+  // side traces of the viscous term: each side's own normal viscous flux
+  // F_v.n sigma (components 1..4; the mass equation has none), evaluated at the
+  // side's own face nodes and averaged on the mortar (oracle/physics.py
+  // NavierStokes.side_flux_traces; DESIGN.md §3 decision 3)
+  static constexpr bool FVTR = true;
+  static constexpr int NTR = 4;
   __device__ static bool viscous(const double* P) { return P[3] > 0.0; }
 
   __device__ static void prim(const double* P, const double* q, double& rho, double& u,
@@ -182,6 +200,40 @@ struct Law<LAW_NS> {
 #pragma unroll
       for (int k = 0; k < 5; ++k) out[k] += n[d] * fv[k];
     }
+  }
+  // F_v.n sigma at a side's own face node (oracle NavierStokes.side_visc_normal
+  // times sigma) from the traces gv of (u, v, w, T) and G of their gradient;
+  // kind < 0: interior or isolated side, else the boundary treatment of
+  // bc_visc_normal.  out[k] = component 1 + k.
+  __device__ static void side_visc(const double* P, const double* gv, const double G[3][NGV],
+                                   const double* n, double sigma, int kind, double* out) {
+    if (kind == BC_SYMMETRY) {
+#pragma unroll
+      for (int k = 0; k < NTR; ++k) out[k] = 0.0;
+      return;
+    }
+    const bool wall = kind == BC_WALL;
+    const double u = wall ? 0.0 : gv[0], v = wall ? 0.0 : gv[1], w = wall ? 0.0 : gv[2];
+    double Gw[3][NGV];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      Gw[d][0] = G[d][0];
+      Gw[d][1] = G[d][1];
+      Gw[d][2] = G[d][2];
+      Gw[d][3] = wall ? 0.0 : G[d][3];
+    }
+    double acc[NTR];
+#pragma unroll
+    for (int k = 0; k < NTR; ++k) acc[k] = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      double fv[5];
+      visc_dir(P, u, v, w, Gw, d, fv);
+#pragma unroll
+      for (int k = 0; k < NTR; ++k) acc[k] += n[d] * fv[1 + k];
+    }
+#pragma unroll
+    for (int k = 0; k < NTR; ++k) out[k] = acc[k] * sigma;
   }
   __device__ static double wave_speed(const double* P, const double* q) {
     double rho, u, v, w, p;

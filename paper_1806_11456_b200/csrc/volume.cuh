@@ -110,6 +110,107 @@ __device__ __forceinline__ void item_side_traces(const DevPlan& P, int slot0, in
   }
 }
 
+// Own-order geometry of an element side at face node kf: sigma and the outward
+// normal ([4][nf] per side; uniform sides read node 0).
+__device__ __forceinline__ void side_geometry(const DevPlan& P, long long so, int nf, int kf, bool uni,
+                                              double& sigma, double* nrm) {
+  const double* geo = P.side_geo + so * 4 + (uni ? 0 : kf);
+  sigma = geo[0];
+  nrm[0] = geo[nf];
+  nrm[1] = geo[2 * nf];
+  nrm[2] = geo[3 * nf];
+}
+
+// Viscous side traces of a work item for laws that carry each side's own
+// normal viscous flux (Law::FVTR; oracle/operators.py apply, side_fv_sigma):
+// one warp per element side evaluates F_v.n sigma at the side's own face nodes
+// from the traces of the lifted variables gvol(e, k, off) and of the gradient
+// Gvol(e, c, off), with the side's boundary treatment in a coupled evaluation.
+// Own-order sides store it in P.gtr; nonconforming sides of a coupled
+// evaluation interpolate it onto the side's mortar (own frame) on the FP64
+// tensor cores, the two values of each lane being exactly its B-operand
+// positions of the first pass, and store it in P.gtrm.
+template <int LAW, class GV, class GG>
+__device__ __forceinline__ void item_side_visc(const DevPlan& P, int slot0, int E, int coupled,
+                                               const int np[3], const int strides[3],
+                                               const double (*bnd)[16], GV gvol, GG Gvol) {
+  using L = Law<LAW>;
+  constexpr int NGV = L::NGV, NTR = L::NTR;
+  const bool lgl = P.family == 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int task = warp; task < E * 6; task += blockDim.x >> 5) {
+    const int e = task / 6, s = task % 6, slot = slot0 + e;
+    int d, a, b;
+    side_dirs(s, d, a, b);
+    const int na = sel3(a, np[0], np[1], np[2]), nb = sel3(b, np[0], np[1], np[2]);
+    const int nd = sel3(d, np[0], np[1], np[2]), nf = na * nb;
+    const int sa = sel3(a, strides[0], strides[1], strides[2]);
+    const int sb = sel3(b, strides[0], strides[1], strides[2]);
+    const int sd = sel3(d, strides[0], strides[1], strides[2]);
+    const int last = (s & 1) ? (nd - 1) * sd : 0;
+    const double* row = bnd[d] + (s & 1) * 8;
+    const long long so = P.side_off[slot * 6 + s];
+    const int fl = P.side_flags[slot * 6 + s];
+    const int kind = coupled ? (fl & 15) - 1 : -1;
+    const bool uni = (fl >> 4) & 1;
+    // F_v.n sigma at own face node (ia, ib)
+    auto fv_at = [&](int ia, int ib, double* out) {
+      const int off0 = ia * sa + ib * sb;
+      double gv[NGV], G[3][NGV];
+      if (lgl) {
+#pragma unroll
+        for (int k = 0; k < NGV; ++k) gv[k] = gvol(e, k, off0 + last);
+#pragma unroll
+        for (int c = 0; c < 3 * NGV; ++c) G[c / NGV][c % NGV] = Gvol(e, c, off0 + last);
+      } else {
+#pragma unroll
+        for (int k = 0; k < NGV; ++k) gv[k] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3 * NGV; ++c) G[c / NGV][c % NGV] = 0.0;
+        for (int m = 0; m < nd; ++m) {
+          const double r = row[m];
+#pragma unroll
+          for (int k = 0; k < NGV; ++k) gv[k] += r * gvol(e, k, off0 + m * sd);
+#pragma unroll
+          for (int c = 0; c < 3 * NGV; ++c) G[c / NGV][c % NGV] += r * Gvol(e, c, off0 + m * sd);
+        }
+      }
+      double sigma, nrm[3];
+      side_geometry(P, so, nf, ia + na * ib, uni, sigma, nrm);
+      L::side_visc(P.prm, gv, G, nrm, sigma, kind, out);
+    };
+    const int4 si = P.side_info[slot * 6 + s];
+    if (coupled && (si.x & 1)) {
+      int ma, mb;
+      side_mortar_dims(si, ma, mb);
+      const int nm = ma * mb;
+      const int g = lane >> 2, q = lane & 3;
+      double v0[NTR], v1[NTR];
+#pragma unroll
+      for (int k = 0; k < NTR; ++k) v0[k] = v1[k] = 0.0;
+      if (g < nb) {
+        if (q < na) fv_at(q, g, v0);
+        if (q + 4 < na) fv_at(q + 4, g, v1);
+      }
+      const double* T1 = P.tables + OFF_T + ((na - 1) * 8 + (ma - 1)) * 64;
+      const double* T2 = P.tables + OFF_T + ((nb - 1) * 8 + (mb - 1)) * 64;
+      double* dst = P.gtrm + (long long)si.w * NTR;
+      warp_proj_mma<NTR>(na, nb, T1, ma, T2, mb,
+                         [&](int c, int ia, int) { return ia < 4 ? v0[c] : v1[c]; },
+                         [&](int c, int A, int B, double x) { dst[(long long)c * nm + A + ma * B] = x; });
+    } else {
+      double* dst = P.gtr + so * NTR;
+      for (int k = lane; k < nf; k += 32) {
+        const int ib = k / na, ia = k - ib * na;
+        double fv[NTR];
+        fv_at(ia, ib, fv);
+#pragma unroll
+        for (int c = 0; c < NTR; ++c) dst[(long long)c * nf + k] = fv[c];
+      }
+    }
+  }
+}
+
 // L2 bulk prefetch of a work item's per-side surface span ([C][nf] per side,
 // contiguous over the item's slots and sides), read late by the scatter.
 template <int C>
@@ -469,8 +570,9 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
     }
   }
   __syncthreads();
-  // stage G in shared memory (reusing gs/js) and write it out
-  double* G = sm;   // [NG][tot]
+  // stage G in shared memory (over js; over gs too unless the side traces
+  // need the lifted variables) and write it out
+  double* G = sm + (L::FVTR ? NGV * tot : 0);   // [NG][tot]
 #pragma unroll
   for (int r = 0; r < NPT; ++r) {
     const int t = threadIdx.x + r * blockDim.x;
@@ -485,12 +587,17 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
     }
   }
   __syncthreads();
-  // gradient traces on the six sides (own order, or mortar order when nonconforming)
+  // viscous traces on the six sides (own order, or mortar order when nonconforming)
   {
     const int np[3] = {n1p, n2p, n3p};
     const int strides[3] = {1, n1p, n1p * n2p};
-    item_side_traces<NG>(P, wi.x, wi.y, coupled, np, strides, T.bnd, P.gtr, P.gtrm,
-                         [&](int e, int c, int off) { return G[c * tot + e * n + off]; });
+    if constexpr (L::FVTR)
+      item_side_visc<LAW>(P, wi.x, wi.y, coupled, np, strides, T.bnd,
+                          [&](int e, int k, int off) { return gs[k * tot + e * n + off]; },
+                          [&](int e, int c, int off) { return G[c * tot + e * n + off]; });
+    else
+      item_side_traces<NG>(P, wi.x, wi.y, coupled, np, strides, T.bnd, P.gtr, P.gtrm,
+                           [&](int e, int c, int off) { return G[c * tot + e * n + off]; });
   }
 }
 
@@ -585,9 +692,27 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
       side_dirs(s, d, a, b);
       if (ijk[d] != ((s & 1) ? np[d] - 1 : 0)) continue;
       const int nf = np[a] * np[b];
-      double* dst = P.gtr + P.side_off[slot * 6 + s] * NG + ijk[a] + np[a] * ijk[b];
+      const int kf = ijk[a] + np[a] * ijk[b];
+      const long long so = P.side_off[slot * 6 + s];
+      if constexpr (L::FVTR) {
+        // this side's own F_v.n sigma at the node (LGL: the traces are the
+        // node's own lifted variables and gradient)
+        const int fl = P.side_flags[slot * 6 + s];
+        double sigma, nrm[3], gv[NGV], G3[3][NGV], fv[L::NTR];
+        side_geometry(P, so, nf, kf, (fl >> 4) & 1, sigma, nrm);
 #pragma unroll
-      for (int c = 0; c < NG; ++c) dst[(long long)c * nf] = x[c];
+        for (int kk = 0; kk < NGV; ++kk) gv[kk] = gs[kk * tot + t];
+#pragma unroll
+        for (int c = 0; c < NG; ++c) G3[c / NGV][c % NGV] = x[c];
+        L::side_visc(P.prm, gv, G3, nrm, sigma, coupled ? (fl & 15) - 1 : -1, fv);
+        double* dst = P.gtr + so * L::NTR + kf;
+#pragma unroll
+        for (int c = 0; c < L::NTR; ++c) dst[(long long)c * nf] = fv[c];
+      } else {
+        double* dst = P.gtr + so * NG + kf;
+#pragma unroll
+        for (int c = 0; c < NG; ++c) dst[(long long)c * nf] = x[c];
+      }
     }
   }
 }
