@@ -258,7 +258,8 @@ int setup_attrs(tdg_plan* p) {
   // The limit is a per-function, process-wide attribute shared by every
   // plan: set it to the MAXN-item bound, never to this plan's (smaller) need.
   const size_t ngv = p->ngv, ng = 3 * ngv, nv = p->nv, b = MAXN * sizeof(double);
-  const size_t lift = (LAW == LAW_NS ? ngv + std::max<size_t>(9, ng) : std::max(ngv + 9, ng)) * b, own = (ngv + std::max<size_t>(9, nv)) * b + 16,
+  const size_t lift = (LAW == LAW_NS ? ngv + std::max<size_t>(9, ng) : std::max(ngv + 9, ng)) * b,
+               own = (ngv + std::max<size_t>(9, nv)) * b + 16 + (ngv + 3) * (LIFT_FACE_NODES + 64 * 6) * sizeof(double),
                flux = 3 * nv * b;
   int rc = with_nx<LAW>(p->iso, [&](auto nx) -> int {
     constexpr int NX = decltype(nx)::value;
@@ -648,13 +649,27 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   }
   const long long item_nodes =
       std::max<long long>(1, std::min<long long>(MAXN, p->nodes / (2LL * nsm_attr)));
+  // g* form of the conforming-face lift (plans served by k_vol_lift_own);
+  // TDG_GSTAR=0 restores the per-side g*·n σ arrays
+  {
+    const char* gsv = getenv("TDG_GSTAR");
+    d.gstar = (desc->family == TDG_LGL && p->viscous && d.ncface > 0 && d.nmface == 0 &&
+               !(gsv && gsv[0] == '0')) ? 1 : 0;
+  }
   std::vector<int2> work;
   for (int s = 0; s < ns;) {
     const int* o = &p->orders_h[3 * s];
     const int n = (o[0] + 1) * (o[1] + 1) * (o[2] + 1);
     // <= MAX_ITEM_ELEMS elements: per-element reductions (tau, dt, norms)
     // use fixed shared-memory arrays of that size
-    const int cap = std::min(MAX_ITEM_ELEMS, std::max(1, static_cast<int>(item_nodes / n)));
+    int cap = std::min(MAX_ITEM_ELEMS, std::max(1, static_cast<int>(item_nodes / n)));
+    // g* form: the lift stages g* and n sigma of the item's face nodes in
+    // shared memory (k_vol_lift_own pass 1); small elements have more face
+    // nodes than volume nodes, so the item is also capped by its face nodes
+    if (d.gstar) {
+      const int per_e = 2 * ((o[1] + 1) * (o[2] + 1) + (o[0] + 1) * (o[2] + 1) + (o[0] + 1) * (o[1] + 1));
+      cap = std::max(1, std::min(cap, LIFT_FACE_NODES / per_e));
+    }
     int e = s;
     while (e < ns && e - s < cap && p->orders_h[3 * e] == o[0] && p->orders_h[3 * e + 1] == o[1] &&
            p->orders_h[3 * e + 2] == o[2])
@@ -767,10 +782,6 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
       tasks = std::max(tasks, w.y * 2 * ((o[1] + 1) * (o[2] + 1) + (o[0] + 1) * (o[2] + 1) + (o[0] + 1) * (o[1] + 1)));
     }
     p->trace_threads = knob("TDG_TRACE_THREADS", d.nmface == 0 && tasks <= 700 ? 128 : ELEM_THREADS);
-    // g* form of the conforming-face lift (plans served by k_vol_lift_own);
-    // TDG_GSTAR=0 restores the per-side g*·n σ arrays
-    d.gstar = (desc->family == TDG_LGL && p->viscous && d.ncface > 0 && d.nmface == 0 &&
-               knob("TDG_GSTAR", 1)) ? 1 : 0;
   }
   d.work = work_d;
   d.work_aff = work_aff_d;
@@ -800,8 +811,18 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     // TMA bulk copy into the region the curved metrics would use (TDG_TMA_Q=0: LDG)
     const char* tq = getenv("TDG_TMA_Q");
     d.tma_q = (!curved && !(tq && tq[0] == '0')) ? 1 : 0;
-    p->smem_lift_own = static_cast<size_t>(p->ngv + (curved ? 9 : 0)) * mt * sizeof(double) +
-                       (d.tma_q ? (static_cast<size_t>(p->nv) * mt + 2) * sizeof(double) : 0);
+    // largest staged g* span over the items ((ngv + 3) values per face node)
+    size_t sfn = 0;
+    if (d.gstar)
+      for (const int2& w : work) {
+        const int* o = &p->orders_h[3 * w.x];
+        const size_t per_e = 2 * ((o[1] + 1) * (o[2] + 1) + (o[0] + 1) * (o[2] + 1) + (o[0] + 1) * (o[1] + 1));
+        sfn = std::max(sfn, ((p->ngv + 3) * per_e * w.y + 1) & ~size_t(1));
+      }
+    const size_t base = static_cast<size_t>(p->ngv + (curved ? 9 : 0)) * mt + sfn;
+    // the Q bulk copy is kept only while three blocks still fit on an SM
+    if (d.tma_q && (base + p->nv * mt + 2) * sizeof(double) > LIFT_OWN_SMEM_3) d.tma_q = 0;
+    p->smem_lift_own = (base + (d.tma_q ? static_cast<size_t>(p->nv) * mt + 2 : 0)) * sizeof(double);
   }
   p->smem_flux = static_cast<size_t>(3 * p->nv) * mt * sizeof(double);
   if (p->viscous) {

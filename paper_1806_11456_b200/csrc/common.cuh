@@ -17,6 +17,10 @@ constexpr int ELEM_THREADS = 256;     // element kernels: 8 warps
 constexpr int MAXN = 512;             // nodes per element work item (<= (7+1)^3)
 constexpr int NPT = MAXN / ELEM_THREADS;
 constexpr int MAX_ITEM_ELEMS = 64;    // elements per work item (per-element smem reductions)
+// k_vol_lift_own (g* form): face nodes of a work item whose g* and n sigma fit
+// beside the item's staged state with three blocks per SM ((4 + 3) x 8 B each)
+constexpr int LIFT_FACE_NODES = 768;
+constexpr size_t LIFT_OWN_SMEM_3 = 72000;       // dynamic shared memory bound for 3 blocks / SM
 constexpr int FACE_THREADS = 64;      // one interior face (<= 8x8 mortar nodes) per block
 constexpr int FACE_THREADS_MAX = 128; // packed uniform faces: face_pack * face_nm <= 128
 constexpr int SIDE_THREADS = 256;     // four element sides per block

@@ -326,11 +326,22 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
 // BR1 lifted gradient at one node (operators.py:224-265): the volume part
 // −Σ_i WD_i(g Ja^i) from the staged g (and Ja on curved items), plus the
 // gathered surface contributions, times M⁻¹.  Shared by both lift kernels.
+// Staged g* form of an item's conforming interior sides (k_vol_lift_own):
+// sf[c][u], c < NGV: g*; c = NGV + d: n_d sigma (signed for this side), at
+// u = e * per_e + (side prefix) + face node; on[e * 6 + side] != 0 marks the
+// sides it serves.
+struct SurfStage {
+  const double* sf;
+  const unsigned char* on;
+  int nfi, per_e;
+};
+
 template <int LAW, int NX, bool GSTAR = false>
 __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T, const double* gs,
                                           const double* js, bool aff, int tot, int n, int n1p,
                                           int n2p, int n3p, int e, int node, int slot, int i, int j,
-                                          int k, double* out /* [3 NGV] */) {
+                                          int k, double* out /* [3 NGV] */,
+                                          const SurfStage& SS = SurfStage{nullptr, nullptr, 0, 0}) {
   using L = Law<LAW>;
   constexpr int NGV = L::NGV, NG = 3 * NGV;
   const int eb = e * n;
@@ -338,49 +349,43 @@ __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T,
 #pragma unroll
   for (int c = 0; c < NG; ++c) acc[c] = 0.0;
   if (aff) {
-    // reference-space weak derivatives of g, then the constant metric transform
+    // reference-space weak derivatives of g (the tangential weights wo_i are
+    // applied with the constant metric transform), then that transform
     double W[3][NGV];
 #pragma unroll
     for (int c = 0; c < 3 * NGV; ++c) W[c / NGV][c % NGV] = 0.0;
-    {
-      const double wo = T.w[1][j] * T.w[2][k];
 #pragma unroll
-      for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
-        if (NX < 0 && m >= n1p) break;
-        const int idx = eb + m + n1p * (j + n2p * k);
-        const double dw = T.dh[0][m * 8 + i] * wo;
+    for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+      if (NX < 0 && m >= n1p) break;
+      const int idx = eb + m + n1p * (j + n2p * k);
+      const double dw = T.dh[0][m * 8 + i];
 #pragma unroll
-        for (int kk = 0; kk < NGV; ++kk) W[0][kk] += dw * gs[kk * tot + idx];
-      }
+      for (int kk = 0; kk < NGV; ++kk) W[0][kk] += dw * gs[kk * tot + idx];
     }
-    {
-      const double wo = T.w[0][i] * T.w[2][k];
 #pragma unroll
-      for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
-        if (NX < 0 && m >= n2p) break;
-        const int idx = eb + i + n1p * (m + n2p * k);
-        const double dw = T.dh[1][m * 8 + j] * wo;
+    for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+      if (NX < 0 && m >= n2p) break;
+      const int idx = eb + i + n1p * (m + n2p * k);
+      const double dw = T.dh[1][m * 8 + j];
 #pragma unroll
-        for (int kk = 0; kk < NGV; ++kk) W[1][kk] += dw * gs[kk * tot + idx];
-      }
+      for (int kk = 0; kk < NGV; ++kk) W[1][kk] += dw * gs[kk * tot + idx];
     }
-    {
-      const double wo = T.w[0][i] * T.w[1][j];
 #pragma unroll
-      for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
-        if (NX < 0 && m >= n3p) break;
-        const int idx = eb + i + n1p * (j + n2p * m);
-        const double dw = T.dh[2][m * 8 + k] * wo;
+    for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
+      if (NX < 0 && m >= n3p) break;
+      const int idx = eb + i + n1p * (j + n2p * m);
+      const double dw = T.dh[2][m * 8 + k];
 #pragma unroll
-        for (int kk = 0; kk < NGV; ++kk) W[2][kk] += dw * gs[kk * tot + idx];
-      }
+      for (int kk = 0; kk < NGV; ++kk) W[2][kk] += dw * gs[kk * tot + idx];
     }
     const double* mj = P.metrics + P.metric_off[slot] + 1;   // Ja^i_d at [3 i + d]
+    const double wi_ = T.w[0][i], wj_ = T.w[1][j], wk_ = T.w[2][k];
+    const double wo3[3] = {wj_ * wk_, wi_ * wk_, wi_ * wj_};
 #pragma unroll
     for (int ii = 0; ii < 3; ++ii) {
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        const double ja = mj[3 * ii + d];
+        const double ja = mj[3 * ii + d] * wo3[ii];
 #pragma unroll
         for (int kk = 0; kk < NGV; ++kk) acc[d * NGV + kk] -= ja * W[ii][kk];
       }
@@ -439,35 +444,22 @@ __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T,
     const int kf = ijk[a] + np[a] * ijk[b];
     const double lw = l * T.w[a][ijk[a]] * T.w[b][ijk[b]];
     if (GSTAR) {
-      const int4 sn = P.side_nb[slot * 6 + s];
-      if (sn.x >= 0) {
-        // conforming interior side: g*·n σ from the face's g* (left frame)
-        // and the left side's σ, n; negated on the right side (exactly the
-        // values k_face<lift> would have stored for this side)
-        int tl = kf;
-        if ((sn.z >> 9) & 1) {
-          const int M1 = sn.z & 7, M2 = (sn.z >> 3) & 7, orient = (sn.z >> 6) & 7;
-          int ap, bp;
-          if (orient & 4) {
-            bp = kf % (M2 + 1);
-            ap = kf / (M2 + 1);
-          } else {
-            ap = kf % (M1 + 1);
-            bp = kf / (M1 + 1);
-          }
-          tl = ((orient & 1) ? M1 - ap : ap) + (M1 + 1) * ((orient & 2) ? M2 - bp : bp);
-        }
-        const double* gv = P.gsf + (long long)sn.x * NGV + tl;
-        const double* geo = P.face_geo + sn.y + (((sn.z >> 10) & 1) ? 0 : tl);
-        const double sg = ((sn.z >> 9) & 1) ? -geo[0] : geo[0];
-        const double nrm[3] = {geo[nf], geo[2 * nf], geo[3 * nf]};
-        double g[NGV];
+      if (SS.on[e * 6 + s]) {
+        // conforming interior side: g* and the side's signed n sigma, staged
+        // per face node by the packed pass of k_vol_lift_own
+        const int nf0 = n2p * n3p, nf1 = n1p * n3p;
+        const int pre = s == 0 ? 0 : s == 1 ? nf0 : s == 2 ? 2 * nf0 : s == 3 ? 2 * nf0 + nf1
+                      : s == 4 ? 2 * (nf0 + nf1) : 2 * (nf0 + nf1) + n1p * n2p;
+        const double* sp = SS.sf + e * SS.per_e + pre + kf;
+        double g[NGV], ns[3];
 #pragma unroll
-        for (int kk = 0; kk < NGV; ++kk) g[kk] = gv[(long long)kk * nf];
+        for (int kk = 0; kk < NGV; ++kk) g[kk] = sp[kk * SS.nfi];
+#pragma unroll
+        for (int d2 = 0; d2 < 3; ++d2) ns[d2] = sp[(NGV + d2) * SS.nfi];
 #pragma unroll
         for (int d2 = 0; d2 < 3; ++d2)
 #pragma unroll
-          for (int kk = 0; kk < NGV; ++kk) acc[d2 * NGV + kk] += lw * (g[kk] * nrm[d2] * sg);
+          for (int kk = 0; kk < NGV; ++kk) acc[d2 * NGV + kk] += lw * (g[kk] * ns[d2]);
         continue;
       }
     }
@@ -601,38 +593,75 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
   }
 }
 
+// Side and face node of the item-local face task u (u < E * per_e): tasks run
+// element by element, side by side (0..5), face node by face node — the order
+// of P.side_off, so u is also the node offset into the item's side arrays.
+__device__ __forceinline__ void face_task(int u, int per_e, int nf0, int nf1, int nf2, int& e, int& s,
+                                          int& kf, int& nf) {
+  e = u / per_e;
+  int r = u - e * per_e;
+  if (r < 2 * nf0) {
+    s = r >= nf0;
+    kf = r - s * nf0;
+    nf = nf0;
+  } else if (r < 2 * (nf0 + nf1)) {
+    r -= 2 * nf0;
+    s = 2 + (r >= nf1);
+    kf = r - (s - 2) * nf1;
+    nf = nf1;
+  } else {
+    r -= 2 * (nf0 + nf1);
+    s = 4 + (r >= nf2);
+    kf = r - (s - 4) * nf2;
+    nf = nf2;
+  }
+}
+
 // BR1 lift for LGL plans whose evaluated sides all use own-order traces (no
 // nonconforming face, or an isolated evaluation): the side traces of G are
-// face-node values, so every node writes its gradient straight to the
-// own-order trace arrays of the sides it lies on (and to ``grad`` when the
-// plan stores it).  No staging of G in shared memory and no second barrier,
-// so each thread keeps one node's values at a time (80 registers, 3 blocks
-// per SM: measured faster than 4 blocks with spills at 64).
+// face-node values.  Three passes over the work item:
+//   1. (g* form) packed over the item's face nodes, one thread per (side,
+//      face node): g* and the side's signed n sigma go to shared memory, so
+//      the per-node surface terms below are a few shared loads (in a warp of
+//      consecutive volume nodes only a few lanes lie on any one side: the
+//      gathers, orientation index math and geometry loads would otherwise
+//      run at an eighth of the lanes, once per side the warp touches);
+//   2. one thread per node: volume part + surface terms, times M^-1 -> grad;
+//   3. packed over the face nodes again: each side's viscous trace (Navier-
+//      Stokes: its own F_v.n sigma) from the gradient just written (read
+//      back through L2) and the staged lifted variables.
 template <int LAW, int NX>
 __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, const double* __restrict__ Q,
                                                                    int coupled) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
+  __shared__ unsigned char side_on[MAX_ITEM_ELEMS * 6];
   extern __shared__ double sm[];
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
+  const int nf0 = n2p * n3p, nf1 = n1p * n3p, nf2 = n1p * n2p;
+  const int per_e = 2 * (nf0 + nf1 + nf2), nfi = wi.y * per_e;
+  const bool gst = coupled && P.gstar;
   double qa[NPT][NV];
   __shared__ unsigned long long qbar;
-  double* gs = sm;               // [NGV][tot]
-  double* js = sm + NGV * tot;   // [9][tot]  (curved items only)
+  // [sf: (NGV + 3) x nfi, g* form only] [gs: NGV x tot] [js: 9 x tot | TMA Q]
+  double* sf = sm;
+  double* gs = sm + (gst ? (((NGV + 3) * nfi + 1) & ~1) : 0);   // [NGV][tot], 16-byte aligned
+  double* js = gs + NGV * tot;                                    // [9][tot]  (curved items only)
   const bool tma = P.tma_q != 0;
+  double* qs = gs + ((NGV * tot + 1) & ~1);   // 16-byte aligned bulk-copy destination
+  int shift = 0;
   if (tma) {
     // the item's slots are contiguous in Q: one bulk copy of [nv][n] x E
     // (16-byte aligned span; data starts `shift` doubles in) into shared
-    // memory after the g region, while the tables are staged
-    double* qs = sm + ((NGV * tot + 1) & ~1);   // 16-byte aligned destination
+    // memory after the g region, while the tables and g* are staged
     const long long n0 = P.node_off[wi.x];
     const double* src = Q + n0 * NV;
-    const int shift = static_cast<int>((reinterpret_cast<unsigned long long>(src) & 15ull) >> 3);
+    shift = static_cast<int>((reinterpret_cast<unsigned long long>(src) & 15ull) >> 3);
     if (threadIdx.x == 0) {
       mbar_init(&qbar, 1);
       mbar_fence_init();
@@ -641,11 +670,44 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
       mbar_expect_tx(&qbar, static_cast<uint32_t>(hi - lo));
       bulk_g2s(qs, reinterpret_cast<const void*>(lo), static_cast<uint32_t>(hi - lo), &qbar);
     }
-    if (coupled && P.gstar)
-      prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
-    else
-      prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
-    load_tables(P, N1, N2, N3, T);
+  } else {
+    load_item_state<NV>(P, Q, wi, n, tot, qa);
+    if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
+  }
+  if (!gst) prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+  if (gst) {
+    // pass 1: g* and n sigma of the conforming interior sides
+    for (int u = threadIdx.x; u < nfi; u += blockDim.x) {
+      int e, s, kf, nf;
+      face_task(u, per_e, nf0, nf1, nf2, e, s, kf, nf);
+      const int4 sn = P.side_nb[(wi.x + e) * 6 + s];
+      if (kf == 0) side_on[e * 6 + s] = sn.x >= 0;
+      if (sn.x < 0) continue;
+      int tl = kf;
+      if ((sn.z >> 9) & 1) {
+        // right side: its face node in the left frame
+        const int M1 = sn.z & 7, M2 = (sn.z >> 3) & 7, orient = (sn.z >> 6) & 7;
+        int ap, bp;
+        if (orient & 4) {
+          bp = kf % (M2 + 1);
+          ap = kf / (M2 + 1);
+        } else {
+          ap = kf % (M1 + 1);
+          bp = kf / (M1 + 1);
+        }
+        tl = ((orient & 1) ? M1 - ap : ap) + (M1 + 1) * ((orient & 2) ? M2 - bp : bp);
+      }
+      const double* gv = P.gsf + (long long)sn.x * NGV + tl;
+      const double* geo = P.face_geo + sn.y + (((sn.z >> 10) & 1) ? 0 : tl);
+      const double sg = ((sn.z >> 9) & 1) ? -geo[0] : geo[0];
+#pragma unroll
+      for (int kk = 0; kk < NGV; ++kk) sf[kk * nfi + u] = gv[(long long)kk * nf];
+#pragma unroll
+      for (int d2 = 0; d2 < 3; ++d2) sf[(NGV + d2) * nfi + u] = geo[(1 + d2) * nf] * sg;
+    }
+  }
+  load_tables(P, N1, N2, N3, T);
+  if (tma) {
     __syncthreads();   // mbarrier initialised before anyone waits on it
     mbar_wait(&qbar, 0);
 #pragma unroll
@@ -657,26 +719,20 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
         for (int v = 0; v < NV; ++v) qa[r][v] = qs[shift + (e * NV + v) * n + node];
       }
     }
-  } else {
-    load_item_state<NV>(P, Q, wi, n, tot, qa);
-    if (coupled && P.gstar)
-      prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
-    else
-      prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
-    if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
-    load_tables(P, N1, N2, N3, T);
   }
   const bool aff = P.work_aff[blockIdx.x] != 0;
   // staging needs no table: one barrier covers both
   stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
   __syncthreads();
+  const SurfStage SS{sf, side_on, nfi, per_e};
+  // pass 2
 #pragma unroll 1
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
     const int e = t / n, node = t - e * n, slot = wi.x + e;
     const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
     double x[NG];
-    if (coupled && P.gstar)
-      lift_node<LAW, NX, true>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+    if (gst)
+      lift_node<LAW, NX, true>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x, SS);
     else
       lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
     if (P.grad) {
@@ -684,35 +740,51 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, con
 #pragma unroll
       for (int c = 0; c < NG; ++c) P.grad[gb + (long long)c * n + node] = x[c];
     }
-    const int ijk[3] = {i, j, k};
-    const int np[3] = {n1p, n2p, n3p};
+    if constexpr (!L::FVTR) {
+      // scalar laws: the side traces are the gradient's face-node values
+      const int ijk[3] = {i, j, k};
+      const int np[3] = {n1p, n2p, n3p};
 #pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      int d, a, b;
-      side_dirs(s, d, a, b);
-      if (ijk[d] != ((s & 1) ? np[d] - 1 : 0)) continue;
-      const int nf = np[a] * np[b];
-      const int kf = ijk[a] + np[a] * ijk[b];
-      const long long so = P.side_off[slot * 6 + s];
-      if constexpr (L::FVTR) {
-        // this side's own F_v.n sigma at the node (LGL: the traces are the
-        // node's own lifted variables and gradient)
-        const int fl = P.side_flags[slot * 6 + s];
-        double sigma, nrm[3], gv[NGV], G3[3][NGV], fv[L::NTR];
-        side_geometry(P, so, nf, kf, (fl >> 4) & 1, sigma, nrm);
-#pragma unroll
-        for (int kk = 0; kk < NGV; ++kk) gv[kk] = gs[kk * tot + t];
-#pragma unroll
-        for (int c = 0; c < NG; ++c) G3[c / NGV][c % NGV] = x[c];
-        L::side_visc(P.prm, gv, G3, nrm, sigma, coupled ? (fl & 15) - 1 : -1, fv);
-        double* dst = P.gtr + so * L::NTR + kf;
-#pragma unroll
-        for (int c = 0; c < L::NTR; ++c) dst[(long long)c * nf] = fv[c];
-      } else {
-        double* dst = P.gtr + so * NG + kf;
+      for (int s = 0; s < 6; ++s) {
+        int d, a, b;
+        side_dirs(s, d, a, b);
+        if (ijk[d] != ((s & 1) ? np[d] - 1 : 0)) continue;
+        const int nf = np[a] * np[b];
+        const int kf = ijk[a] + np[a] * ijk[b];
+        double* dst = P.gtr + P.side_off[slot * 6 + s] * NG + kf;
 #pragma unroll
         for (int c = 0; c < NG; ++c) dst[(long long)c * nf] = x[c];
       }
+    }
+  }
+  if constexpr (L::FVTR) {
+    // pass 3: this side's own F_v.n sigma at each face node (LGL: the traces
+    // are the node's own lifted variables and gradient)
+    __syncthreads();   // the block's gradient stores are visible to the block
+    const long long so0 = P.side_off[wi.x * 6];
+    for (int u = threadIdx.x; u < nfi; u += blockDim.x) {
+      int e, s, kf, nf;
+      face_task(u, per_e, nf0, nf1, nf2, e, s, kf, nf);
+      const int slot = wi.x + e;
+      int d, a, b;
+      side_dirs(s, d, a, b);
+      const int na = sel3(a, n1p, n2p, n3p), nd = sel3(d, n1p, n2p, n3p);
+      const int ib = kf / na, ia = kf - ib * na;
+      const int off = ia * sel3(a, 1, n1p, n1p * n2p) + ib * sel3(b, 1, n1p, n1p * n2p) +
+                      ((s & 1) ? (nd - 1) * sel3(d, 1, n1p, n1p * n2p) : 0);
+      const long long so = so0 + u - kf;
+      const int fl = P.side_flags[slot * 6 + s];
+      double sigma, nrm[3], gv[NGV], G3[3][NGV], fv[L::NTR];
+      const double* gp = P.grad + P.node_off[slot] * NG + off;
+#pragma unroll
+      for (int c = 0; c < NG; ++c) G3[c / NGV][c % NGV] = __ldcg(gp + (long long)c * n);
+      side_geometry(P, so, nf, kf, (fl >> 4) & 1, sigma, nrm);
+#pragma unroll
+      for (int kk = 0; kk < NGV; ++kk) gv[kk] = gs[kk * tot + e * n + off];
+      L::side_visc(P.prm, gv, G3, nrm, sigma, coupled ? (fl & 15) - 1 : -1, fv);
+      double* dst = P.gtr + so * L::NTR + kf;
+#pragma unroll
+      for (int c = 0; c < L::NTR; ++c) dst[(long long)c * nf] = fv[c];
     }
   }
 }
@@ -810,37 +882,43 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
         F0[v] = F1[v] = F2[v] = 0.0;
       }
       {
-        const double wo = T.w[1][j] * T.w[2][k];
 #pragma unroll
         for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
           if (NX < 0 && m >= n1p) break;
           const int idx = eb + m + n1p * (j + n2p * k);
-          const double dw = T.dh[0][m * 8 + i] * wo;
+          const double dw = T.dh[0][m * 8 + i];
 #pragma unroll
           for (int v = 0; v < NV; ++v) F0[v] += dw * ft[(0 * NV + v) * tot + idx];
         }
+        const double wo = T.w[1][j] * T.w[2][k];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) F0[v] *= wo;
       }
       {
-        const double wo = T.w[0][i] * T.w[2][k];
 #pragma unroll
         for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
           if (NX < 0 && m >= n2p) break;
           const int idx = eb + i + n1p * (m + n2p * k);
-          const double dw = T.dh[1][m * 8 + j] * wo;
+          const double dw = T.dh[1][m * 8 + j];
 #pragma unroll
           for (int v = 0; v < NV; ++v) F1[v] += dw * ft[(1 * NV + v) * tot + idx];
         }
+        const double wo = T.w[0][i] * T.w[2][k];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) F1[v] *= wo;
       }
       {
-        const double wo = T.w[0][i] * T.w[1][j];
 #pragma unroll
         for (int m = 0; m < (NX >= 0 ? NX + 1 : 8); ++m) {
           if (NX < 0 && m >= n3p) break;
           const int idx = eb + i + n1p * (j + n2p * m);
-          const double dw = T.dh[2][m * 8 + k] * wo;
+          const double dw = T.dh[2][m * 8 + k];
 #pragma unroll
           for (int v = 0; v < NV; ++v) F2[v] += dw * ft[(2 * NV + v) * tot + idx];
         }
+        const double wo = T.w[0][i] * T.w[1][j];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) F2[v] *= wo;
       }
 #pragma unroll
       for (int v = 0; v < NV; ++v) F[v] -= (F0[v] + F1[v]) + F2[v];
