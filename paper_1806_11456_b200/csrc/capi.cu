@@ -802,8 +802,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   // dynamic shared memory sized by the largest work item (<= MAXN nodes)
   const size_t mt = static_cast<size_t>(p->max_tot);
   // (Navier-Stokes keeps the lifted variables beside G for the side traces)
-  p->smem_lift = static_cast<size_t>(desc->law == TDG_LAW_NS ? p->ngv + std::max(9, NG)
-                                                             : std::max(p->ngv + 9, NG)) * mt * sizeof(double);
+  p->smem_lift = static_cast<size_t>(p->ngv + 9) * mt * sizeof(double);
   {
     bool curved = false;
     for (int s = 0; s < ns && !curved; ++s) curved = desc->affine[s] == 0;

@@ -551,45 +551,32 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const d
 
   __syncthreads();
 
-  double Greg[NPT][NG];
+  // one node at a time: the gradient goes straight to P.grad (always stored
+  // when the lift runs), so no value is held across a barrier
+#pragma unroll 1
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int e = t / n, node = t - e * n, slot = wi.x + e;
+    const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+    double x[NG];
+    lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+    const long long gb = P.node_off[slot] * NG;
 #pragma unroll
-  for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * blockDim.x;
-    if (t < tot) {
-      const int e = t / n, node = t - e * n, slot = wi.x + e;
-      const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
-      lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, Greg[r]);
-    }
+    for (int c = 0; c < NG; ++c) P.grad[gb + (long long)c * n + node] = x[c];
   }
-  __syncthreads();
-  // stage G in shared memory (over js; over gs too unless the side traces
-  // need the lifted variables) and write it out
-  double* G = sm + (L::FVTR ? NGV * tot : 0);   // [NG][tot]
-#pragma unroll
-  for (int r = 0; r < NPT; ++r) {
-    const int t = threadIdx.x + r * blockDim.x;
-    if (t < tot) {
-      const int e = t / n, node = t - e * n, slot = wi.x + e;
-      const long long gb = P.node_off[slot] * NG;
-#pragma unroll
-      for (int c = 0; c < NG; ++c) {
-        G[c * tot + t] = Greg[r][c];
-        if (P.grad) P.grad[gb + (long long)c * n + node] = Greg[r][c];
-      }
-    }
-  }
-  __syncthreads();
-  // viscous traces on the six sides (own order, or mortar order when nonconforming)
+  __syncthreads();   // the block's gradient stores are visible to the block
+  // viscous traces on the six sides (own order, or mortar order when
+  // nonconforming), the gradient read back through L2
   {
     const int np[3] = {n1p, n2p, n3p};
     const int strides[3] = {1, n1p, n1p * n2p};
+    auto Gvol = [&](int e, int c, int off) {
+      return __ldcg(P.grad + P.node_off[wi.x + e] * NG + (long long)c * n + off);
+    };
     if constexpr (L::FVTR)
       item_side_visc<LAW>(P, wi.x, wi.y, coupled, np, strides, T.bnd,
-                          [&](int e, int k, int off) { return gs[k * tot + e * n + off]; },
-                          [&](int e, int c, int off) { return G[c * tot + e * n + off]; });
+                          [&](int e, int k, int off) { return gs[k * tot + e * n + off]; }, Gvol);
     else
-      item_side_traces<NG>(P, wi.x, wi.y, coupled, np, strides, T.bnd, P.gtr, P.gtrm,
-                           [&](int e, int c, int off) { return G[c * tot + e * n + off]; });
+      item_side_traces<NG>(P, wi.x, wi.y, coupled, np, strides, T.bnd, P.gtr, P.gtrm, Gvol);
   }
 }
 
