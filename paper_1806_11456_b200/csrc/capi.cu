@@ -167,7 +167,7 @@ struct tdg_plan {
   const double* traces_of = nullptr;
   bool rk_traces = false;   // LGL, no nonconforming face
   size_t smem_lift = 0, smem_flux = 0;
-  int elem_threads = ELEM_THREADS;   // block size of the lift / flux kernels
+  int elem_threads = VOL_THREADS;   // block size of the lift / flux kernels
   int max_tot = MAXN;                // largest work item (nodes)
   int trace_threads = ELEM_THREADS;  // k_trace_q block size
   int64_t side_nodes = 0;
@@ -258,7 +258,8 @@ int setup_attrs(tdg_plan* p) {
   // The limit is a per-function, process-wide attribute shared by every
   // plan: set it to the MAXN-item bound, never to this plan's (smaller) need.
   const size_t ngv = p->ngv, ng = 3 * ngv, nv = p->nv, b = MAXN * sizeof(double);
-  const size_t lift = (LAW == LAW_NS ? ngv + std::max<size_t>(9, ng) : std::max(ngv + 9, ng)) * b,
+  // k_vol_lift: [ngv + 9] per node, or [ngv] per node + [ntr] per face node (<= 1536 per item)
+  const size_t lift = std::max<size_t>((ngv + std::max<size_t>(9, ng)) * b, ngv * b + ng * 1536 * sizeof(double)),
                own = (ngv + std::max<size_t>(9, nv)) * b + 16 + (ngv + 3) * (LIFT_FACE_NODES + 64 * 6) * sizeof(double),
                flux = 3 * nv * b;
   int rc = with_nx<LAW>(p->iso, [&](auto nx) -> int {
@@ -685,7 +686,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     max_tot = std::max<long long>(max_tot, static_cast<long long>(w.y) * (o[0] + 1) * (o[1] + 1) * (o[2] + 1));
   }
   p->elem_threads = static_cast<int>(std::min<long long>(
-      ELEM_THREADS, std::max<long long>(128, (max_tot + NPT * 32 - 1) / (NPT * 32) * 32)));
+      VOL_THREADS, std::max<long long>(128, (max_tot + NPT * 32 - 1) / (NPT * 32) * 32)));
   p->max_tot = static_cast<int>(max_tot);
   std::vector<int4> iso, bnd;
   iso.reserve(6 * ns);
@@ -802,7 +803,18 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   // dynamic shared memory sized by the largest work item (<= MAXN nodes)
   const size_t mt = static_cast<size_t>(p->max_tot);
   // (Navier-Stokes keeps the lifted variables beside G for the side traces)
-  p->smem_lift = static_cast<size_t>(p->ngv + 9) * mt * sizeof(double);
+  {
+    // lifted variables + max(curved metric staging, the item's side values of
+    // the packed viscous-trace pass ([ntr] per face node))
+    size_t need = static_cast<size_t>(p->ngv + 9) * mt;
+    for (const int2& w : work) {
+      const int* o = &p->orders_h[3 * w.x];
+      const size_t n = static_cast<size_t>(o[0] + 1) * (o[1] + 1) * (o[2] + 1);
+      const size_t per_e = 2 * ((o[1] + 1) * (o[2] + 1) + (o[0] + 1) * (o[2] + 1) + (o[0] + 1) * (o[1] + 1));
+      need = std::max(need, p->ngv * n * w.y + p->ntr * per_e * w.y);
+    }
+    p->smem_lift = need * sizeof(double);
+  }
   {
     bool curved = false;
     for (int s = 0; s < ns && !curved; ++s) curved = desc->affine[s] == 0;
@@ -1343,3 +1355,14 @@ int tdg_prolong_add(const tdg_transfer* t, const double* Qc, const double* Qc0, 
 }
 
 }  // extern "C"
+
+#ifdef TDG_PHASE_CLOCK
+extern "C" int tdg_debug_phases(unsigned long long* out32, int reset) {
+  if (out32) cudaMemcpyFromSymbol(out32, tdg::g_phase, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(tdg::g_phase, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -15,7 +15,15 @@ constexpr int TABLES_LEN = OFF_T + PAD * PAD * PAD * PAD;
 
 constexpr int ELEM_THREADS = 256;     // element kernels: 8 warps
 constexpr int MAXN = 512;             // nodes per element work item (<= (7+1)^3)
-constexpr int NPT = MAXN / ELEM_THREADS;
+#ifndef TDG_VOL_THREADS
+#define TDG_VOL_THREADS 256
+#endif
+#ifndef TDG_VOL_BLOCKS
+#define TDG_VOL_BLOCKS 3
+#endif
+constexpr int VOL_THREADS = TDG_VOL_THREADS;   // lift / flux kernels: threads per block ...
+constexpr int VOL_BLOCKS = TDG_VOL_BLOCKS;     // ... and resident blocks per SM (register cap)
+constexpr int NPT = MAXN / VOL_THREADS;        // nodes per thread of a full work item
 constexpr int MAX_ITEM_ELEMS = 64;    // elements per work item (per-element smem reductions)
 // k_vol_lift_own (g* form): face nodes of a work item whose g* and n sigma fit
 // beside the item's staged state with three blocks per SM ((4 + 3) x 8 B each)

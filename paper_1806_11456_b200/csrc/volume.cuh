@@ -12,6 +12,17 @@
 
 namespace tdg {
 
+#ifdef TDG_PHASE_CLOCK
+__device__ unsigned long long g_phase[32];
+#define PHASE_T(k) do { if (threadIdx.x == 0) pt[k] = clock64(); } while (0)
+#define PHASE_DECL long long pt[8] = {0,0,0,0,0,0,0,0}
+#define PHASE_END(base, n) do { if (threadIdx.x == 0) { for (int z = 1; z < n; ++z) atomicAdd(&g_phase[base + z], (unsigned long long)(pt[z] - pt[z-1])); atomicAdd(&g_phase[base], 1ull);} } while (0)
+#else
+#define PHASE_T(k)
+#define PHASE_DECL
+#define PHASE_END(base, n)
+#endif
+
 struct ElemTables {
   double dh[3][64];   // Dhat[m*8+i] per direction
   double w[3][8];
@@ -119,96 +130,6 @@ __device__ __forceinline__ void side_geometry(const DevPlan& P, long long so, in
   nrm[0] = geo[nf];
   nrm[1] = geo[2 * nf];
   nrm[2] = geo[3 * nf];
-}
-
-// Viscous side traces of a work item for laws that carry each side's own
-// normal viscous flux (Law::FVTR; oracle/operators.py apply, side_fv_sigma):
-// one warp per element side evaluates F_v.n sigma at the side's own face nodes
-// from the traces of the lifted variables gvol(e, k, off) and of the gradient
-// Gvol(e, c, off), with the side's boundary treatment in a coupled evaluation.
-// Own-order sides store it in P.gtr; nonconforming sides of a coupled
-// evaluation interpolate it onto the side's mortar (own frame) on the FP64
-// tensor cores, the two values of each lane being exactly its B-operand
-// positions of the first pass, and store it in P.gtrm.
-template <int LAW, class GV, class GG>
-__device__ __forceinline__ void item_side_visc(const DevPlan& P, int slot0, int E, int coupled,
-                                               const int np[3], const int strides[3],
-                                               const double (*bnd)[16], GV gvol, GG Gvol) {
-  using L = Law<LAW>;
-  constexpr int NGV = L::NGV, NTR = L::NTR;
-  const bool lgl = P.family == 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int task = warp; task < E * 6; task += blockDim.x >> 5) {
-    const int e = task / 6, s = task % 6, slot = slot0 + e;
-    int d, a, b;
-    side_dirs(s, d, a, b);
-    const int na = sel3(a, np[0], np[1], np[2]), nb = sel3(b, np[0], np[1], np[2]);
-    const int nd = sel3(d, np[0], np[1], np[2]), nf = na * nb;
-    const int sa = sel3(a, strides[0], strides[1], strides[2]);
-    const int sb = sel3(b, strides[0], strides[1], strides[2]);
-    const int sd = sel3(d, strides[0], strides[1], strides[2]);
-    const int last = (s & 1) ? (nd - 1) * sd : 0;
-    const double* row = bnd[d] + (s & 1) * 8;
-    const long long so = P.side_off[slot * 6 + s];
-    const int fl = P.side_flags[slot * 6 + s];
-    const int kind = coupled ? (fl & 15) - 1 : -1;
-    const bool uni = (fl >> 4) & 1;
-    // F_v.n sigma at own face node (ia, ib)
-    auto fv_at = [&](int ia, int ib, double* out) {
-      const int off0 = ia * sa + ib * sb;
-      double gv[NGV], G[3][NGV];
-      if (lgl) {
-#pragma unroll
-        for (int k = 0; k < NGV; ++k) gv[k] = gvol(e, k, off0 + last);
-#pragma unroll
-        for (int c = 0; c < 3 * NGV; ++c) G[c / NGV][c % NGV] = Gvol(e, c, off0 + last);
-      } else {
-#pragma unroll
-        for (int k = 0; k < NGV; ++k) gv[k] = 0.0;
-#pragma unroll
-        for (int c = 0; c < 3 * NGV; ++c) G[c / NGV][c % NGV] = 0.0;
-        for (int m = 0; m < nd; ++m) {
-          const double r = row[m];
-#pragma unroll
-          for (int k = 0; k < NGV; ++k) gv[k] += r * gvol(e, k, off0 + m * sd);
-#pragma unroll
-          for (int c = 0; c < 3 * NGV; ++c) G[c / NGV][c % NGV] += r * Gvol(e, c, off0 + m * sd);
-        }
-      }
-      double sigma, nrm[3];
-      side_geometry(P, so, nf, ia + na * ib, uni, sigma, nrm);
-      L::side_visc(P.prm, gv, G, nrm, sigma, kind, out);
-    };
-    const int4 si = P.side_info[slot * 6 + s];
-    if (coupled && (si.x & 1)) {
-      int ma, mb;
-      side_mortar_dims(si, ma, mb);
-      const int nm = ma * mb;
-      const int g = lane >> 2, q = lane & 3;
-      double v0[NTR], v1[NTR];
-#pragma unroll
-      for (int k = 0; k < NTR; ++k) v0[k] = v1[k] = 0.0;
-      if (g < nb) {
-        if (q < na) fv_at(q, g, v0);
-        if (q + 4 < na) fv_at(q + 4, g, v1);
-      }
-      const double* T1 = P.tables + OFF_T + ((na - 1) * 8 + (ma - 1)) * 64;
-      const double* T2 = P.tables + OFF_T + ((nb - 1) * 8 + (mb - 1)) * 64;
-      double* dst = P.gtrm + (long long)si.w * NTR;
-      warp_proj_mma<NTR>(na, nb, T1, ma, T2, mb,
-                         [&](int c, int ia, int) { return ia < 4 ? v0[c] : v1[c]; },
-                         [&](int c, int A, int B, double x) { dst[(long long)c * nm + A + ma * B] = x; });
-    } else {
-      double* dst = P.gtr + so * NTR;
-      for (int k = lane; k < nf; k += 32) {
-        const int ib = k / na, ia = k - ib * na;
-        double fv[NTR];
-        fv_at(ia, ib, fv);
-#pragma unroll
-        for (int c = 0; c < NTR; ++c) dst[(long long)c * nf + k] = fv[c];
-      }
-    }
-  }
 }
 
 // L2 bulk prefetch of a work item's per-side surface span ([C][nf] per side,
@@ -518,68 +439,6 @@ __device__ __forceinline__ void stage_grad_vars(const DevPlan& P, int2 wi, int n
   }
 }
 
-// ---------------------------------------------------------------------------
-// BR1 lift, volume part + scatter of the face contributions, times M^-1
-// (operators.py:224-265); writes the gradient and its side traces.
-//
-// NX >= 0: compile-time isotropic order (the plan is one (NX,NX,NX) bucket),
-// so index math folds and the contractions unroll; NX = -1: runtime orders.
-// Work items whose elements are all affine take the reference-gradient path:
-// -sum_i Ja^i_d WD_i(g) with the element's constant Ja (no per-node metrics).
-template <int LAW, int NX>
-__global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift(DevPlan P, const double* __restrict__ Q,
-                                                          int coupled) {
-  using L = Law<LAW>;
-  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
-  __shared__ ElemTables T;
-  extern __shared__ double sm[];
-  const int2 wi = P.work[blockIdx.x];
-  const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
-  const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
-  const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
-  const int n = n1p * n2p * n3p, tot = wi.y * n;
-  double qa[NPT][NV];
-  load_item_state<NV>(P, Q, wi, n, tot, qa);
-  prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
-  if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
-  load_tables(P, N1, N2, N3, T);
-  const bool aff = P.work_aff[blockIdx.x] != 0;
-  double* gs = sm;               // [NGV][tot]
-  double* js = sm + NGV * tot;   // [9][tot]  (curved items only)
-  // staging needs no table: one barrier covers both
-  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
-
-  __syncthreads();
-
-  // one node at a time: the gradient goes straight to P.grad (always stored
-  // when the lift runs), so no value is held across a barrier
-#pragma unroll 1
-  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
-    const int e = t / n, node = t - e * n, slot = wi.x + e;
-    const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
-    double x[NG];
-    lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
-    const long long gb = P.node_off[slot] * NG;
-#pragma unroll
-    for (int c = 0; c < NG; ++c) P.grad[gb + (long long)c * n + node] = x[c];
-  }
-  __syncthreads();   // the block's gradient stores are visible to the block
-  // viscous traces on the six sides (own order, or mortar order when
-  // nonconforming), the gradient read back through L2
-  {
-    const int np[3] = {n1p, n2p, n3p};
-    const int strides[3] = {1, n1p, n1p * n2p};
-    auto Gvol = [&](int e, int c, int off) {
-      return __ldcg(P.grad + P.node_off[wi.x + e] * NG + (long long)c * n + off);
-    };
-    if constexpr (L::FVTR)
-      item_side_visc<LAW>(P, wi.x, wi.y, coupled, np, strides, T.bnd,
-                          [&](int e, int k, int off) { return gs[k * tot + e * n + off]; }, Gvol);
-    else
-      item_side_traces<NG>(P, wi.x, wi.y, coupled, np, strides, T.bnd, P.gtr, P.gtrm, Gvol);
-  }
-}
-
 // Side and face node of the item-local face task u (u < E * per_e): tasks run
 // element by element, side by side (0..5), face node by face node — the order
 // of P.side_off, so u is also the node offset into the item's side arrays.
@@ -604,6 +463,154 @@ __device__ __forceinline__ void face_task(int u, int per_e, int nf0, int nf1, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// BR1 lift, volume part + scatter of the face contributions, times M^-1
+// (operators.py:224-265); writes the gradient and its side traces.
+//
+// NX >= 0: compile-time isotropic order (the plan is one (NX,NX,NX) bucket),
+// so index math folds and the contractions unroll; NX = -1: runtime orders.
+// Work items whose elements are all affine take the reference-gradient path:
+// -sum_i Ja^i_d WD_i(g) with the element's constant Ja (no per-node metrics).
+template <int LAW, int NX>
+__global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift(DevPlan P, const double* __restrict__ Q,
+                                                          int coupled) {
+  using L = Law<LAW>;
+  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
+  __shared__ ElemTables T;
+  extern __shared__ double sm[];
+  const int2 wi = P.work[blockIdx.x];
+  const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
+  const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
+  const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
+  const int n = n1p * n2p * n3p, tot = wi.y * n;
+  double qa[NPT][NV];
+  PHASE_DECL;
+  PHASE_T(0);
+  load_item_state<NV>(P, Q, wi, n, tot, qa);
+  prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+  if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
+  load_tables(P, N1, N2, N3, T);
+  const bool aff = P.work_aff[blockIdx.x] != 0;
+  double* gs = sm;               // [NGV][tot]
+  double* js = sm + NGV * tot;   // [9][tot]  (curved items only)
+  // staging needs no table: one barrier covers both
+  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
+  PHASE_T(1);
+  __syncthreads();
+  PHASE_T(2);
+  // one node at a time: the gradient goes straight to P.grad (always stored
+  // when the lift runs), so no value is held across a barrier
+#pragma unroll 1
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int e = t / n, node = t - e * n, slot = wi.x + e;
+    const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+    double x[NG];
+    lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+    const long long gb = P.node_off[slot] * NG;
+#pragma unroll
+    for (int c = 0; c < NG; ++c) P.grad[gb + (long long)c * n + node] = x[c];
+  }
+  PHASE_T(3);
+  __syncthreads();   // the block's gradient stores are visible to the block
+  PHASE_T(4);
+  // viscous traces on the six sides (own order, or mortar order when
+  // nonconforming), the gradient read back through L2
+  const int np[3] = {n1p, n2p, n3p};
+  const int strides[3] = {1, n1p, n1p * n2p};
+  auto Gvol = [&](int e, int c, int off) {
+    return __ldcg(P.grad + P.node_off[wi.x + e] * NG + (long long)c * n + off);
+  };
+  if constexpr (L::FVTR) {
+    // (a) packed over the item's face nodes, one thread per (side, face node):
+    // the side's own F_v.n sigma.  Sides on own-order traces store it; the
+    // nonconforming sides of a coupled evaluation leave it in shared memory
+    // (over the metric staging, dead by now) for (b).  A warp-per-side pass
+    // would walk ~5 dependent memory round trips per side with most lanes idle.
+    constexpr int NTR = L::NTR;
+    const bool lgl = P.family == 1;
+    const int nf0 = n2p * n3p, nf1 = n1p * n3p, nf2 = n1p * n2p;
+    const int per_e = 2 * (nf0 + nf1 + nf2), nfi = wi.y * per_e;
+    double* fvs = sm + NGV * tot;   // [NTR][nfi]
+    const long long so0 = P.side_off[wi.x * 6];
+    for (int u = threadIdx.x; u < nfi; u += blockDim.x) {
+      int e, s, kf, nf;
+      face_task(u, per_e, nf0, nf1, nf2, e, s, kf, nf);
+      const int slot = wi.x + e;
+      int d, a, b;
+      side_dirs(s, d, a, b);
+      const int na = sel3(a, n1p, n2p, n3p), nd = sel3(d, n1p, n2p, n3p);
+      const int sd = sel3(d, strides[0], strides[1], strides[2]);
+      const int ib = kf / na, ia = kf - ib * na;
+      const int off0 = ia * sel3(a, strides[0], strides[1], strides[2]) +
+                       ib * sel3(b, strides[0], strides[1], strides[2]);
+      const int fl = P.side_flags[slot * 6 + s];
+      const int4 si = P.side_info[slot * 6 + s];
+      const long long so = so0 + u - kf;
+      double gv[NGV], G3[3][NGV], fv[NTR], sigma, nrm[3];
+      if (lgl) {
+        const int off = off0 + ((s & 1) ? (nd - 1) * sd : 0);
+#pragma unroll
+        for (int c = 0; c < NG; ++c) G3[c / NGV][c % NGV] = Gvol(e, c, off);
+#pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) gv[kk] = gs[kk * tot + e * n + off];
+      } else {
+        const double* row = T.bnd[d] + (s & 1) * 8;
+#pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) gv[kk] = 0.0;
+#pragma unroll
+        for (int c = 0; c < NG; ++c) G3[c / NGV][c % NGV] = 0.0;
+        for (int m = 0; m < nd; ++m) {
+          const double r = row[m];
+#pragma unroll
+          for (int kk = 0; kk < NGV; ++kk) gv[kk] += r * gs[kk * tot + e * n + off0 + m * sd];
+#pragma unroll
+          for (int c = 0; c < NG; ++c) G3[c / NGV][c % NGV] += r * Gvol(e, c, off0 + m * sd);
+        }
+      }
+      side_geometry(P, so, nf, kf, (fl >> 4) & 1, sigma, nrm);
+      L::side_visc(P.prm, gv, G3, nrm, sigma, coupled ? (fl & 15) - 1 : -1, fv);
+      if (coupled && (si.x & 1)) {
+#pragma unroll
+        for (int c = 0; c < NTR; ++c) fvs[c * nfi + u] = fv[c];
+      } else {
+        double* dst = P.gtr + so * NTR + kf;
+#pragma unroll
+        for (int c = 0; c < NTR; ++c) dst[(long long)c * nf] = fv[c];
+      }
+    }
+    if (coupled && P.nmface > 0) {
+      PHASE_T(5);
+      __syncthreads();
+      PHASE_T(6);
+      // (b) one warp per nonconforming side: interpolate its values onto the
+      // side's mortar (own frame) on the FP64 tensor cores
+      const int warp = threadIdx.x >> 5;
+      for (int task = warp; task < wi.y * 6; task += blockDim.x >> 5) {
+        const int e = task / 6, s = task - 6 * e;
+        const int4 si = P.side_info[(wi.x + e) * 6 + s];
+        if (!(si.x & 1)) continue;
+        int d, a, b;
+        side_dirs(s, d, a, b);
+        const int na = sel3(a, n1p, n2p, n3p), nb = sel3(b, n1p, n2p, n3p);
+        int ma, mb;
+        side_mortar_dims(si, ma, mb);
+        const int nm = ma * mb;
+        const int ub = e * per_e + (d == 0 ? 0 : d == 1 ? 2 * nf0 : 2 * (nf0 + nf1)) + (s & 1) * na * nb;
+        const double* T1 = P.tables + OFF_T + ((na - 1) * 8 + (ma - 1)) * 64;
+        const double* T2 = P.tables + OFF_T + ((nb - 1) * 8 + (mb - 1)) * 64;
+        double* dst = P.gtrm + (long long)si.w * NTR;
+        warp_proj_mma<NTR>(na, nb, T1, ma, T2, mb,
+                           [&](int c, int ia, int ib) { return fvs[c * nfi + ub + ia + na * ib]; },
+                           [&](int c, int A, int B, double x) { dst[(long long)c * nm + A + ma * B] = x; });
+      }
+    }
+  } else {
+    item_side_traces<NG>(P, wi.x, wi.y, coupled, np, strides, T.bnd, P.gtr, P.gtrm, Gvol);
+  }
+  PHASE_T(7);
+  PHASE_END(0, 8);
+}
+
 // BR1 lift for LGL plans whose evaluated sides all use own-order traces (no
 // nonconforming face, or an isolated evaluation): the side traces of G are
 // face-node values.  Three passes over the work item:
@@ -618,7 +625,7 @@ __device__ __forceinline__ void face_task(int u, int per_e, int nf0, int nf1, in
 //      Stokes: its own F_v.n sigma) from the gradient just written (read
 //      back through L2) and the staged lifted variables.
 template <int LAW, int NX>
-__global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_lift_own(DevPlan P, const double* __restrict__ Q,
+__global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own(DevPlan P, const double* __restrict__ Q,
                                                                    int coupled) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
@@ -796,7 +803,7 @@ struct FluxArgs {
 };
 
 template <int LAW, int MODE, int NX>
-__global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
+__global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_flux(DevPlan P, const double* Q, FluxArgs A) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   __shared__ ElemTables T;
@@ -819,6 +826,8 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
   const int n = n1p * n2p * n3p, tot = wi.y * n;
   double* ft = sm;   // [3][NV][tot]
   const bool visc = L::viscous(P.prm);
+  PHASE_DECL;
+  PHASE_T(0);
   // the contravariant fluxes need no table: they are formed first, the
   // tables are staged after them, and one barrier covers both
 #pragma unroll 1
@@ -852,8 +861,9 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
     }
   }
   load_tables(P, N1, N2, N3, T);
+  PHASE_T(1);
   __syncthreads();
-
+  PHASE_T(2);
   double rmax = 0.0;
 #pragma unroll 1
   for (int r = 0; r < NPT; ++r) {
@@ -993,9 +1003,12 @@ __global__ void __launch_bounds__(ELEM_THREADS, 3) k_vol_flux(DevPlan P, const d
       }
     }
   }
+  PHASE_T(3);
   if (MODE == MODE_R || (MODE == MODE_RK)) {
     if (A.norm && (MODE == MODE_R || A.stage == 0)) block_max_to(rmax, A.norm, T.red);
   }
+  PHASE_T(4);
+  PHASE_END(8, 5);
   if (MODE == MODE_TAU) {
     __syncthreads();
     for (int e = threadIdx.x; e < wi.y; e += blockDim.x)
