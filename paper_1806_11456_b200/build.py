@@ -44,7 +44,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = True) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", *SOURCES]
+    extra = os.environ.get("TDG_NVCC_EXTRA", "").split()   # e.g. -DTDG_PHASE_CLOCK (development builds)
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", *SOURCES]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

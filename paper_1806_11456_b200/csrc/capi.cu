@@ -267,6 +267,7 @@ int setup_attrs(tdg_plan* p) {
     int r;
     if ((r = allow_smem(k_vol_lift<LAW, NX>, lift))) return r;
     if ((r = allow_smem(k_vol_lift_own<LAW, NX>, own))) return r;
+    if ((r = allow_smem(k_vol_lift_own_inl<LAW, NX>, own))) return r;
     if ((r = allow_smem(k_vol_flux<LAW, MODE_A, NX>, flux))) return r;
     if ((r = allow_smem(k_vol_flux<LAW, MODE_R, NX>, flux))) return r;
     if ((r = allow_smem(k_vol_flux<LAW, MODE_RK, NX>, flux))) return r;
@@ -338,8 +339,10 @@ int run_surface(tdg_plan* p, const DevPlan& d, const double* Q, int isolated, cu
       const bool own = d.family == TDG_LGL && (isolated || d.nmface == 0);
       with_nx<LAW>(p->iso, [&](auto nx) -> int {
         constexpr int NX = decltype(nx)::value;
-        if (own)
+        if (own && d.lift_packed)
           k_vol_lift_own<LAW, NX><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q, coupled);
+        else if (own)
+          k_vol_lift_own_inl<LAW, NX><<<d.nwork, p->elem_threads, p->smem_lift_own, st>>>(d, Q, coupled);
         else
           k_vol_lift<LAW, NX><<<d.nwork, p->elem_threads, p->smem_lift, st>>>(d, Q, coupled);
         return 0;
@@ -657,6 +660,22 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     d.gstar = (desc->family == TDG_LGL && p->viscous && d.ncface > 0 && d.nmface == 0 &&
                !(gsv && gsv[0] == '0')) ? 1 : 0;
   }
+  // own-order lift variant: packed face-node passes on affine plans and on
+  // curved plans of order >= 4 (measured: config 4 V-cycle 60.2 ms packed at
+  // every level, 62.5 ms in-loop; config 5, curved N = 3: 26.2 ms in-loop,
+  // 28.1 ms packed); TDG_LIFT_PACKED_MIN overrides the smallest order
+  {
+    bool any_curved = false;
+    for (int s = 0; s < ns && !any_curved; ++s) any_curved = desc->affine[s] == 0;
+    const char* pm = getenv("TDG_LIFT_PACKED_MIN");
+    const int pmin = pm ? atoi(pm) : (any_curved ? 4 : 1);
+    int omin = 99;
+    for (int s = 0; s < ns; ++s)
+      for (int dd = 0; dd < 3; ++dd) omin = std::min(omin, p->orders_h[3 * s + dd]);
+    d.lift_packed = (ns > 0 && omin >= pmin) ? 1 : 0;
+  }
+  int lift_face_nodes = LIFT_FACE_NODES;
+  if (const char* v = getenv("TDG_LIFT_FACE_NODES")) lift_face_nodes = std::min(LIFT_FACE_NODES, std::max(24, atoi(v)));
   std::vector<int2> work;
   for (int s = 0; s < ns;) {
     const int* o = &p->orders_h[3 * s];
@@ -667,9 +686,9 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     // g* form: the lift stages g* and n sigma of the item's face nodes in
     // shared memory (k_vol_lift_own pass 1); small elements have more face
     // nodes than volume nodes, so the item is also capped by its face nodes
-    if (d.gstar) {
+    if (d.gstar && d.lift_packed) {
       const int per_e = 2 * ((o[1] + 1) * (o[2] + 1) + (o[0] + 1) * (o[2] + 1) + (o[0] + 1) * (o[1] + 1));
-      cap = std::max(1, std::min(cap, LIFT_FACE_NODES / per_e));
+      cap = std::max(1, std::min(cap, lift_face_nodes / per_e));
     }
     int e = s;
     while (e < ns && e - s < cap && p->orders_h[3 * e] == o[0] && p->orders_h[3 * e + 1] == o[1] &&
@@ -824,7 +843,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
     d.tma_q = (!curved && !(tq && tq[0] == '0')) ? 1 : 0;
     // largest staged g* span over the items ((ngv + 3) values per face node)
     size_t sfn = 0;
-    if (d.gstar)
+    if (d.gstar && d.lift_packed)
       for (const int2& w : work) {
         const int* o = &p->orders_h[3 * w.x];
         const size_t per_e = 2 * ((o[1] + 1) * (o[2] + 1) + (o[0] + 1) * (o[2] + 1) + (o[0] + 1) * (o[1] + 1));
@@ -832,7 +851,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
       }
     const size_t base = static_cast<size_t>(p->ngv + (curved ? 9 : 0)) * mt + sfn;
     // the Q bulk copy is kept only while three blocks still fit on an SM
-    if (d.tma_q && (base + p->nv * mt + 2) * sizeof(double) > LIFT_OWN_SMEM_3) d.tma_q = 0;
+    if (d.tma_q && d.lift_packed && (base + p->nv * mt + 2) * sizeof(double) > LIFT_OWN_SMEM_3) d.tma_q = 0;
     p->smem_lift_own = (base + (d.tma_q ? static_cast<size_t>(p->nv) * mt + 2 : 0)) * sizeof(double);
   }
   p->smem_flux = static_cast<size_t>(3 * p->nv) * mt * sizeof(double);

@@ -110,6 +110,7 @@ struct DevPlan {
   // the left side's trace offset) instead of g*·n σ for both sides (2 x 3 ngv),
   // and k_vol_lift_own forms g*·n σ from it and the face geometry
   int gstar;
+  int lift_packed;   // own-order lift: packed face-node passes (k_vol_lift_own) or in-loop (k_vol_lift_own_inl)
   double* gsf;    // [side_nodes][ngv] (left-side offsets used)
   // per element side (slot*6+side) of a conforming interior face: x = the
   // left side's trace offset (nodes; -1 otherwise), y = face-geometry

@@ -164,8 +164,16 @@ __global__ void __launch_bounds__(FACE_THREADS_MAX) k_face(DevPlan P) {
 // and L2-projects them onto both sides on the FP64 tensor cores (the right
 // side negated and re-oriented).  Nothing goes through HBM between the
 // pointwise evaluation and the projections (operators.py:211-217, 330-334).
+#ifndef TDG_MORTAR_BLOCKS_FLUX
+#define TDG_MORTAR_BLOCKS_FLUX 16   // resident one-warp blocks per SM (register cap 65536 / 32 / blocks)
+#endif
+#ifndef TDG_MORTAR_BLOCKS_LIFT
+#define TDG_MORTAR_BLOCKS_LIFT 20
+#endif
 template <int LAW, bool FLUX>
-__global__ void __launch_bounds__(32 * MORTAR_WARPS, (FLUX ? 4 : 5) * 4 / MORTAR_WARPS) k_mortar(DevPlan P) {
+__global__ void __launch_bounds__(32 * MORTAR_WARPS,
+                                  (FLUX ? TDG_MORTAR_BLOCKS_FLUX : TDG_MORTAR_BLOCKS_LIFT) / MORTAR_WARPS)
+k_mortar(DevPlan P) {
   using L = Law<LAW>;
   constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
   constexpr int COUT = FLUX ? NV : NG;

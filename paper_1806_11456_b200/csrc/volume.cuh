@@ -257,7 +257,7 @@ struct SurfStage {
   int nfi, per_e;
 };
 
-template <int LAW, int NX, bool GSTAR = false>
+template <int LAW, int NX, int GSTAR = 0>
 __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T, const double* gs,
                                           const double* js, bool aff, int tot, int n, int n1p,
                                           int n2p, int n3p, int e, int node, int slot, int i, int j,
@@ -364,7 +364,40 @@ __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T,
     const int nf = np[a] * np[b];
     const int kf = ijk[a] + np[a] * ijk[b];
     const double lw = l * T.w[a][ijk[a]] * T.w[b][ijk[b]];
-    if (GSTAR) {
+    if (GSTAR == 2) {
+      const int4 sn = P.side_nb[slot * 6 + s];
+      if (sn.x >= 0) {
+        // conforming interior side: g*·n σ from the face's g* (left frame)
+        // and the left side's σ, n; negated on the right side (exactly the
+        // values k_face<lift> would have stored for this side)
+        int tl = kf;
+        if ((sn.z >> 9) & 1) {
+          const int M1 = sn.z & 7, M2 = (sn.z >> 3) & 7, orient = (sn.z >> 6) & 7;
+          int ap, bp;
+          if (orient & 4) {
+            bp = kf % (M2 + 1);
+            ap = kf / (M2 + 1);
+          } else {
+            ap = kf % (M1 + 1);
+            bp = kf / (M1 + 1);
+          }
+          tl = ((orient & 1) ? M1 - ap : ap) + (M1 + 1) * ((orient & 2) ? M2 - bp : bp);
+        }
+        const double* gv = P.gsf + (long long)sn.x * NGV + tl;
+        const double* geo = P.face_geo + sn.y + (((sn.z >> 10) & 1) ? 0 : tl);
+        const double sg = ((sn.z >> 9) & 1) ? -geo[0] : geo[0];
+        const double nrm[3] = {geo[nf], geo[2 * nf], geo[3 * nf]};
+        double g[NGV];
+#pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) g[kk] = gv[(long long)kk * nf];
+#pragma unroll
+        for (int d2 = 0; d2 < 3; ++d2)
+#pragma unroll
+          for (int kk = 0; kk < NGV; ++kk) acc[d2 * NGV + kk] += lw * (g[kk] * nrm[d2] * sg);
+        continue;
+      }
+    }
+    if (GSTAR == 1) {
       if (SS.on[e * 6 + s]) {
         // conforming interior side: g* and the side's signed n sigma, staged
         // per face node by the packed pass of k_vol_lift_own
@@ -726,7 +759,7 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own(DevPla
     const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
     double x[NG];
     if (gst)
-      lift_node<LAW, NX, true>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x, SS);
+      lift_node<LAW, NX, 1>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x, SS);
     else
       lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
     if (P.grad) {
@@ -779,6 +812,123 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own(DevPla
       double* dst = P.gtr + so * L::NTR + kf;
 #pragma unroll
       for (int c = 0; c < L::NTR; ++c) dst[(long long)c * nf] = fv[c];
+    }
+  }
+}
+
+// In-loop variant of k_vol_lift_own for low orders (P.lift_packed == 0):
+// every node gathers its sides' g* and geometry itself and writes its own
+// side traces.  With more face nodes than volume nodes per element (N <= 3)
+// the two packed passes of k_vol_lift_own cost more than the divergence they
+// remove (config 5, N = 3 curved: V-cycle 26.2 ms in-loop, 28.1 ms packed;
+// config 4, N = 7: lift 0.59 ms in-loop, 0.55 ms packed).  No staging of G in shared memory and no second barrier,
+// so each thread keeps one node's values at a time (80 registers, 3 blocks
+// per SM: measured faster than 4 blocks with spills at 64).
+template <int LAW, int NX>
+__global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own_inl(DevPlan P, const double* __restrict__ Q,
+                                                                   int coupled) {
+  using L = Law<LAW>;
+  constexpr int NV = L::NV, NGV = L::NGV, NG = 3 * NGV;
+  __shared__ ElemTables T;
+  extern __shared__ double sm[];
+  const int2 wi = P.work[blockIdx.x];
+  const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
+  const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
+  const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
+  const int n = n1p * n2p * n3p, tot = wi.y * n;
+  double qa[NPT][NV];
+  __shared__ unsigned long long qbar;
+  double* gs = sm;               // [NGV][tot]
+  double* js = sm + NGV * tot;   // [9][tot]  (curved items only)
+  const bool tma = P.tma_q != 0;
+  if (tma) {
+    // the item's slots are contiguous in Q: one bulk copy of [nv][n] x E
+    // (16-byte aligned span; data starts `shift` doubles in) into shared
+    // memory after the g region, while the tables are staged
+    double* qs = sm + ((NGV * tot + 1) & ~1);   // 16-byte aligned destination
+    const long long n0 = P.node_off[wi.x];
+    const double* src = Q + n0 * NV;
+    const int shift = static_cast<int>((reinterpret_cast<unsigned long long>(src) & 15ull) >> 3);
+    if (threadIdx.x == 0) {
+      mbar_init(&qbar, 1);
+      mbar_fence_init();
+      const unsigned long long a = reinterpret_cast<unsigned long long>(src);
+      const unsigned long long lo = a & ~15ull, hi = (a + 8ull * NV * tot + 15ull) & ~15ull;
+      mbar_expect_tx(&qbar, static_cast<uint32_t>(hi - lo));
+      bulk_g2s(qs, reinterpret_cast<const void*>(lo), static_cast<uint32_t>(hi - lo), &qbar);
+    }
+    if (coupled && P.gstar)
+      prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
+    else
+      prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+    load_tables(P, N1, N2, N3, T);
+    __syncthreads();   // mbarrier initialised before anyone waits on it
+    mbar_wait(&qbar, 0);
+#pragma unroll
+    for (int r = 0; r < NPT; ++r) {
+      const int t = threadIdx.x + r * blockDim.x;
+      if (t < tot) {
+        const int e = t / n, node = t - e * n;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) qa[r][v] = qs[shift + (e * NV + v) * n + node];
+      }
+    }
+  } else {
+    load_item_state<NV>(P, Q, wi, n, tot, qa);
+    if (coupled && P.gstar)
+      prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
+    else
+      prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
+    if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
+    load_tables(P, N1, N2, N3, T);
+  }
+  const bool aff = P.work_aff[blockIdx.x] != 0;
+  // staging needs no table: one barrier covers both
+  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
+  __syncthreads();
+#pragma unroll 1
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int e = t / n, node = t - e * n, slot = wi.x + e;
+    const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+    double x[NG];
+    if (coupled && P.gstar)
+      lift_node<LAW, NX, 2>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+    else
+      lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
+    if (P.grad) {
+      const long long gb = P.node_off[slot] * NG;
+#pragma unroll
+      for (int c = 0; c < NG; ++c) P.grad[gb + (long long)c * n + node] = x[c];
+    }
+    const int ijk[3] = {i, j, k};
+    const int np[3] = {n1p, n2p, n3p};
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      int d, a, b;
+      side_dirs(s, d, a, b);
+      if (ijk[d] != ((s & 1) ? np[d] - 1 : 0)) continue;
+      const int nf = np[a] * np[b];
+      const int kf = ijk[a] + np[a] * ijk[b];
+      const long long so = P.side_off[slot * 6 + s];
+      if constexpr (L::FVTR) {
+        // this side's own F_v.n sigma at the node (LGL: the traces are the
+        // node's own lifted variables and gradient)
+        const int fl = P.side_flags[slot * 6 + s];
+        double sigma, nrm[3], gv[NGV], G3[3][NGV], fv[L::NTR];
+        side_geometry(P, so, nf, kf, (fl >> 4) & 1, sigma, nrm);
+#pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) gv[kk] = gs[kk * tot + t];
+#pragma unroll
+        for (int c = 0; c < NG; ++c) G3[c / NGV][c % NGV] = x[c];
+        L::side_visc(P.prm, gv, G3, nrm, sigma, coupled ? (fl & 15) - 1 : -1, fv);
+        double* dst = P.gtr + so * L::NTR + kf;
+#pragma unroll
+        for (int c = 0; c < L::NTR; ++c) dst[(long long)c * nf] = fv[c];
+      } else {
+        double* dst = P.gtr + so * NG + kf;
+#pragma unroll
+        for (int c = 0; c < NG; ++c) dst[(long long)c * nf] = x[c];
+      }
     }
   }
 }
