@@ -158,6 +158,12 @@ NS_CASES = [
     ("rotated_jitter", "random1_4", "LGL", "curl"),
     ("bc_box", "random1_4", "LGL", "curl"),
     ("bc_box", "uniform3", "LG", "curl"),
+    # own-order lift, packed face-node passes: curved conforming N = 4 (staged
+    # g* with per-node geometry), the same with boundary sides, and an affine
+    # plan with several elements per work item (bulk-copied state)
+    ("periodic_jitter", "uniform4", "LGL", "curl"),
+    ("bc_box", "uniform4", "LGL", "curl"),
+    ("periodic_affine", "uniform2", "LGL", "curl"),
 ]
 
 
@@ -179,8 +185,8 @@ def _ns_mesh(kind):
 
 def _orders(kind, nel, seed=11):
     rng = np.random.default_rng(seed)
-    if kind == "uniform3":
-        return np.full((nel, 3), 3)
+    if kind.startswith("uniform"):
+        return np.full((nel, 3), int(kind[len("uniform"):]))
     lo, hi = (int(v) for v in kind.replace("random", "").split("_"))
     return rng.integers(lo, hi + 1, (nel, 3))
 
@@ -195,6 +201,25 @@ def test_navier_stokes_matches_oracle(mesh_kind, orders_kind, family, form):
         # the non-periodic direction carries a freestream far field on other tags
         msh.bc.setdefault("boundary", "freestream")
     _compare_case(msh, law, _orders(orders_kind, msh.num_elements), family, form)
+
+
+@pytest.mark.parametrize("mesh_kind,orders_kind,packed_min", [
+    ("periodic_affine", "uniform3", "9"),   # affine plan forced onto the in-loop lift
+    ("periodic_jitter", "uniform3", "1"),   # curved N = 3 forced onto the packed lift
+    ("bc_box", "uniform3", "1"),            # ... with wall / symmetry / far-field sides
+])
+def test_own_order_lift_variants_match_oracle(monkeypatch, mesh_kind, orders_kind, packed_min):
+    """Both variants of the own-order lift (k_vol_lift_own: packed passes;
+    k_vol_lift_own_inl: in-loop) on plans where the default rule would pick the
+    other one (the plan reads TDG_LIFT_PACKED_MIN when it is created)."""
+    from paper_1806_11456_b200 import physics
+
+    monkeypatch.setenv("TDG_LIFT_PACKED_MIN", packed_min)
+    msh = _ns_mesh(mesh_kind)
+    if mesh_kind == "bc_box":
+        msh.bc.setdefault("boundary", "freestream")
+    law = physics.NavierStokes(mach=0.3, reynolds=100.0)
+    _compare_case(msh, law, _orders(orders_kind, msh.num_elements), "LGL", "curl")
 
 
 @pytest.mark.parametrize("family", ["LG", "LGL"])
