@@ -180,10 +180,13 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // One warp projects C component arrays of (na x nb) values to (ma x mb):
 //   out[c][A, B] = sum_b T2[B][b] sum_a T1[A][a] in[c][a, b]      (T rows stride 8)
 // on the FP64 tensor cores, one zero-padded 8x8 tile per component and pass:
-// pass 1 (M = A, K = a, N = b) takes its B operand straight from ld(c, a, b);
-// its result stays in registers and reaches pass 2 (M = B, K = b, N = A)
-// through quad shuffles.  No shared memory, no __syncwarp; the whole warp
-// must be converged.  st(c, A, B, value) receives each output once.
+// pass 1 (M = A, K = a, N = b) takes its B operand straight from ld(c, a, b).
+// Its result tmp[A][b] leaves lane (g, q) holding tmp[g][2q] and tmp[g][2q+1],
+// which are exactly the B operands B[k][n = g] of pass 2 (M = B, K = b, N = A)
+// if its two k-steps run over the even and the odd b: step 0 pairs k = q with
+// b = 2q, step 1 with b = 2q + 1, and T2 is read in the same order.  Nothing
+// moves between lanes.  No shared memory, no __syncwarp; the whole warp must
+// be converged.  st(c, A, B, value) receives each output once.
 template <int C, class Load, class Store>
 __device__ __forceinline__ void warp_proj_mma(int na, int nb, const double* __restrict__ T1, int ma,
                                               const double* __restrict__ T2, int mb, Load ld,
@@ -192,12 +195,9 @@ __device__ __forceinline__ void warp_proj_mma(int na, int nb, const double* __re
   const int g = lane >> 2, q = lane & 3;
   const double t10 = (g < ma && q < na) ? T1[g * 8 + q] : 0.0;
   const double t11 = (g < ma && q + 4 < na) ? T1[g * 8 + q + 4] : 0.0;
-  const double t20 = (g < mb && q < nb) ? T2[g * 8 + q] : 0.0;
-  const double t21 = (g < mb && q + 4 < nb) ? T2[g * 8 + q + 4] : 0.0;
-  const bool ka = na > 4, kb = nb > 4;
-  // pass-2 operand tmp[A = g][b = q (+4)] sits in lane (g, q/2 (+2)), element q&1
-  const int s0 = (g << 2) | (q >> 1), s1 = s0 + 2;
-  const bool odd = q & 1;
+  const double t20 = (g < mb && 2 * q < nb) ? T2[g * 8 + 2 * q] : 0.0;
+  const double t21 = (g < mb && 2 * q + 1 < nb) ? T2[g * 8 + 2 * q + 1] : 0.0;
+  const bool ka = na > 4, kb = nb > 1;
   const bool colv = g < nb;
 #pragma unroll
   for (int c = 0; c < C; ++c) {
@@ -207,14 +207,8 @@ __device__ __forceinline__ void warp_proj_mma(int na, int nb, const double* __re
     dmma_8x8x4(d0, d1, t10, b0);
     if (ka) dmma_8x8x4(d0, d1, t11, b1);
     double o0 = 0.0, o1 = 0.0;
-    {
-      const double e0 = __shfl_sync(0xffffffffu, d0, s0), e1 = __shfl_sync(0xffffffffu, d1, s0);
-      dmma_8x8x4(o0, o1, t20, odd ? e1 : e0);
-    }
-    if (kb) {
-      const double e0 = __shfl_sync(0xffffffffu, d0, s1), e1 = __shfl_sync(0xffffffffu, d1, s1);
-      dmma_8x8x4(o0, o1, t21, odd ? e1 : e0);
-    }
+    dmma_8x8x4(o0, o1, t20, d0);
+    if (kb) dmma_8x8x4(o0, o1, t21, d1);
     if (g < mb) {
       if (2 * q < ma) st(c, 2 * q, g, o0);
       if (2 * q + 1 < ma) st(c, 2 * q + 1, g, o1);
