@@ -186,11 +186,13 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // if its two k-steps run over the even and the odd b: step 0 pairs k = q with
 // b = 2q, step 1 with b = 2q + 1, and T2 is read in the same order.  Nothing
 // moves between lanes.  No shared memory, no __syncwarp; the whole warp must
-// be converged.  st(c, A, B, value) receives each output once.
-template <int C, class Load, class Store>
+// be converged.  Output (A, B) of component c is stored once, as
+// out[c * cstride + idx(A, B)] (negated if NEG): the two offsets and their
+// predicates of a lane are formed once, outside the component loop.
+template <int C, bool NEG = false, class Load, class Index>
 __device__ __forceinline__ void warp_proj_mma(int na, int nb, const double* __restrict__ T1, int ma,
                                               const double* __restrict__ T2, int mb, Load ld,
-                                              Store st) {
+                                              double* __restrict__ out, long long cstride, Index idx) {
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, q = lane & 3;
   const double t10 = (g < ma && q < na) ? T1[g * 8 + q] : 0.0;
@@ -199,6 +201,9 @@ __device__ __forceinline__ void warp_proj_mma(int na, int nb, const double* __re
   const double t21 = (g < mb && 2 * q + 1 < nb) ? T2[g * 8 + 2 * q + 1] : 0.0;
   const bool ka = na > 4, kb = nb > 1;
   const bool colv = g < nb;
+  const bool p0 = g < mb && 2 * q < ma, p1 = g < mb && 2 * q + 1 < ma;
+  double* const out0 = out + (p0 ? idx(2 * q, g) : 0);
+  double* const out1 = out + (p1 ? idx(2 * q + 1, g) : 0);
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     double d0 = 0.0, d1 = 0.0;
@@ -209,10 +214,8 @@ __device__ __forceinline__ void warp_proj_mma(int na, int nb, const double* __re
     double o0 = 0.0, o1 = 0.0;
     dmma_8x8x4(o0, o1, t20, d0);
     if (kb) dmma_8x8x4(o0, o1, t21, d1);
-    if (g < mb) {
-      if (2 * q < ma) st(c, 2 * q, g, o0);
-      if (2 * q + 1 < ma) st(c, 2 * q + 1, g, o1);
-    }
+    if (p0) out0[c * cstride] = NEG ? -o0 : o0;
+    if (p1) out1[c * cstride] = NEG ? -o1 : o1;
   }
 }
 

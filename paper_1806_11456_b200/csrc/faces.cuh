@@ -209,17 +209,15 @@ k_mortar(DevPlan P) {
     double* out = surf + (long long)fo.y * COUT;
     const int nf = (L1 + 1) * (L2 + 1);
     warp_proj_mma<COUT>(M1 + 1, M2 + 1, P.tables + OFF_T + (M1 * 8 + L1) * 64, L1 + 1,
-                        P.tables + OFF_T + (M2 * 8 + L2) * 64, L2 + 1, ld,
-                        [&](int c, int A, int B, double x) { out[(long long)c * nf + A + (L1 + 1) * B] = x; });
+                        P.tables + OFF_T + (M2 * 8 + L2) * 64, L2 + 1, ld, out, nf,
+                        [&](int A, int B) { return A + (L1 + 1) * B; });
   }
   {
     double* out = surf + (long long)fo.z * COUT;
     const int nf = (R1 + 1) * (R2 + 1);
-    warp_proj_mma<COUT>(M1 + 1, M2 + 1, P.tables + OFF_T + (M1 * 8 + R1) * 64, R1 + 1,
-                        P.tables + OFF_T + (M2 * 8 + R2) * 64, R2 + 1, ld,
-                        [&](int c, int A, int B, double x) {
-                          out[(long long)c * nf + right_index(A, B, R1, R2, orient)] = -x;
-                        });
+    warp_proj_mma<COUT, true>(M1 + 1, M2 + 1, P.tables + OFF_T + (M1 * 8 + R1) * 64, R1 + 1,
+                              P.tables + OFF_T + (M2 * 8 + R2) * 64, R2 + 1, ld, out, nf,
+                              [&](int A, int B) { return right_index(A, B, R1, R2, orient); });
   }
   // look-ahead L2 prefetch, issued after this warp's own work so that its
   // dependent descriptor loads do not stall the projections

@@ -108,9 +108,7 @@ __device__ __forceinline__ void item_side_traces(const DevPlan& P, int slot0, in
       const double* T1 = P.tables + OFF_T + ((na - 1) * 8 + (ma - 1)) * 64;
       const double* T2 = P.tables + OFF_T + ((nb - 1) * 8 + (mb - 1)) * 64;
       double* dst = mort + (long long)si.w * C;
-      warp_proj_mma<C>(na, nb, T1, ma, T2, mb, tr, [&](int c, int A, int B, double x) {
-        dst[(long long)c * nm + A + ma * B] = x;
-      });
+      warp_proj_mma<C>(na, nb, T1, ma, T2, mb, tr, dst, nm, [&](int A, int B) { return A + ma * B; });
     } else {
       double* dst = own + P.side_off[slot * 6 + s] * C;
       for (int k = lane; k < nf; k += 32) {
@@ -633,8 +631,8 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift(DevPlan P,
         const double* T2 = P.tables + OFF_T + ((nb - 1) * 8 + (mb - 1)) * 64;
         double* dst = P.gtrm + (long long)si.w * NTR;
         warp_proj_mma<NTR>(na, nb, T1, ma, T2, mb,
-                           [&](int c, int ia, int ib) { return fvs[c * nfi + ub + ia + na * ib]; },
-                           [&](int c, int A, int B, double x) { dst[(long long)c * nm + A + ma * B] = x; });
+                           [&](int c, int ia, int ib) { return fvs[c * nfi + ub + ia + na * ib]; }, dst, nm,
+                           [&](int A, int B) { return A + ma * B; });
       }
     }
   } else {
