@@ -521,6 +521,11 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.law = desc->law;
   d.family = desc->family;
   std::memcpy(d.prm, desc->params, sizeof(d.prm));
+  if (desc->law == TDG_LAW_NS && d.prm[3] > 0.0) {
+    // uniform constants of the viscous flux, formed once (laws.cuh visc_dir)
+    d.prm[4] = 1.0 / d.prm[3];
+    d.prm[5] = 1.0 / ((d.prm[0] - 1.0) * d.prm[1] * d.prm[2] * d.prm[2]);
+  }
   d.nslots = ns;
   d.nfaces = desc->nfaces;
   d.nbfaces = desc->nbfaces;

@@ -5,7 +5,7 @@
 // (mu = 1 non-dimensional, BR1 on (u, v, w, T), Roe flux without entropy fix,
 // mean-of-sides interface viscous flux).  Parameters (plan prm[8]):
 //   advdiff: a, b, c, mu        burgers: bx, by, bz, mu
-//   NS:      gamma, Pr, M, Re (Re = 0: inviscid)          prm[7] = mu_cfl
+//   NS:      gamma, Pr, M, Re (Re = 0: inviscid), [4] = 1/Re, [5] = 1/((gamma-1) Pr M^2)   prm[7] = mu_cfl
 #pragma once
 #include "common.cuh"
 
@@ -123,22 +123,29 @@ struct Law<LAW_NS> {
   static constexpr int NTR = 4;
   __device__ static bool viscous(const double* P) { return P[3] > 0.0; }
 
+  // ir = 1 / rho is formed once per state and reused wherever the oracle
+  // divides by rho (one FP64 division is ~20 instructions)
   __device__ static void prim(const double* P, const double* q, double& rho, double& u,
-                              double& v, double& w, double& p) {
+                              double& v, double& w, double& p, double& ir) {
     rho = q[0];
-    const double ir = 1.0 / rho;
+    ir = 1.0 / rho;
     u = q[1] * ir;
     v = q[2] * ir;
     w = q[3] * ir;
     p = (P[0] - 1.0) * (q[4] - 0.5 * rho * (u * u + v * v + w * w));
   }
+  __device__ static void prim(const double* P, const double* q, double& rho, double& u,
+                              double& v, double& w, double& p) {
+    double ir;
+    prim(P, q, rho, u, v, w, p, ir);
+  }
   __device__ static void grad_vars(const double* P, const double* q, double* g) {
-    double rho, u, v, w, p;
-    prim(P, q, rho, u, v, w, p);
+    double rho, u, v, w, p, ir;
+    prim(P, q, rho, u, v, w, p, ir);
     g[0] = u;
     g[1] = v;
     g[2] = w;
-    g[3] = P[0] * P[2] * P[2] * p / rho;
+    g[3] = P[0] * P[2] * P[2] * p * ir;
   }
   __device__ static void adv_flux(const double* P, const double* q, double f[3][NV]) {
     double rho, u, v, w, p;
@@ -159,8 +166,8 @@ struct Law<LAW_NS> {
   // viscous flux (1/Re)[0, tau_d., u.tau_d + kappa T_d] in direction d
   __device__ static void visc_dir(const double* P, double u, double v, double w,
                                   const double G[3][NGV], int d, double* fv) {
-    const double inv_re = 1.0 / P[3];
-    const double kappa = 1.0 / ((P[0] - 1.0) * P[1] * P[2] * P[2]);
+    const double inv_re = P[4];   // 1 / Re and 1 / ((gamma - 1) Pr M^2), set by tdg_plan_create
+    const double kappa = P[5];
     const double div = G[0][0] + G[1][1] + G[2][2];
     double tau[3];
 #pragma unroll
@@ -244,14 +251,14 @@ struct Law<LAW_NS> {
   __device__ static void riemann(const double* P, const double* ql, const double* qr,
                                  const double* n, double* F) {
     const double g = P[0];
-    double rl, ul, vl, wl, pl, rr, ur, vr, wr, pr;
-    prim(P, ql, rl, ul, vl, wl, pl);
-    prim(P, qr, rr, ur, vr, wr, pr);
+    double rl, ul, vl, wl, pl, rr, ur, vr, wr, pr, irl, irr;
+    prim(P, ql, rl, ul, vl, wl, pl, irl);
+    prim(P, qr, rr, ur, vr, wr, pr, irr);
     const double nx = n[0], ny = n[1], nz = n[2];
     const double vnl = ul * nx + vl * ny + wl * nz;
     const double vnr = ur * nx + vr * ny + wr * nz;
-    const double Hl = (ql[4] + pl) / rl;
-    const double Hr = (qr[4] + pr) / rr;
+    const double Hl = (ql[4] + pl) * irl;
+    const double Hr = (qr[4] + pr) * irr;
     const double sl = sqrt(rl), sr = sqrt(rr);
     const double inv = 1.0 / (sl + sr);
     const double ut = (sl * ul + sr * ur) * inv;
@@ -266,9 +273,10 @@ struct Law<LAW_NS> {
     const double drho = rr - rl, dp = pr - pl;
     const double du = ur - ul, dv = vr - vl, dw = wr - wl;
     const double dvn = vnr - vnl;
-    const double a1 = (dp - rt * ct * dvn) / (2.0 * c2);
-    const double a2 = drho - dp / c2;
-    const double a5 = (dp + rt * ct * dvn) / (2.0 * c2);
+    const double ic2 = 1.0 / c2, hic2 = 0.5 * ic2;
+    const double a1 = (dp - rt * ct * dvn) * hic2;
+    const double a2 = drho - dp * ic2;
+    const double a5 = (dp + rt * ct * dvn) * hic2;
     const double l1 = fabs(vnt - ct), l2 = fabs(vnt), l5 = fabs(vnt + ct);
     const double sx = du - dvn * nx, sy = dv - dvn * ny, sz = dw - dvn * nz;
     double D[5];
