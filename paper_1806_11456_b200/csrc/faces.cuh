@@ -52,8 +52,7 @@ __device__ __forceinline__ void face_point(const DevPlan& P, const double* qsrc,
   }
   if (!FLUX) {
     double gl[NGV], gr[NGV];
-    L::grad_vars(P.prm, ql, gl);
-    L::grad_vars(P.prm, qr, gr);
+    L::grad_vars2(P.prm, ql, qr, gl, gr);
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
@@ -139,8 +138,7 @@ __global__ void __launch_bounds__(FACE_THREADS_MAX) k_face(DevPlan P) {
       ql[v] = P.qtr[tL * NV + (long long)v * nm + t];
       qr[v] = P.qtr[tR * NV + (long long)v * nm + kR];
     }
-    L::grad_vars(P.prm, ql, gl);
-    L::grad_vars(P.prm, qr, gr);
+    L::grad_vars2(P.prm, ql, qr, gl, gr);
     double* dst = P.gsf + tL * NGV + t;
 #pragma unroll
     for (int k = 0; k < NGV; ++k) dst[(long long)k * nm] = 0.5 * (gl[k] + gr[k]);
