@@ -747,6 +747,13 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   std::vector<int> work_ord(3 * work.size());
   for (size_t k = 0; k < work.size(); ++k)
     for (int dd = 0; dd < 3; ++dd) work_ord[3 * k + dd] = p->orders_h[3 * work[k].x + dd];
+  std::vector<int> work_mul(8 * work.size(), 0);
+  for (size_t k = 0; k < work.size(); ++k) {
+    const int a = work_ord[3 * k] + 1, b = work_ord[3 * k + 1] + 1, c = work_ord[3 * k + 2] + 1;
+    const int dv[5] = {a * b * c, a, b, a * b, 2 * (b * c + a * c + a * b)};
+    for (int j = 0; j < 5; ++j) work_mul[8 * k + j] = mdiv_mul(dv[j]);
+  }
+  int* work_mul_d = nullptr;
   int2* work_d;
   int* work_aff_d = nullptr;
   int* work_ord_d = nullptr;
@@ -755,6 +762,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   if (!rc) rc = p->mem.upload(work_aff.data(), work_aff.size(), &work_aff_d);
   if (!rc && ns > 0) rc = p->mem.upload(sflags.data(), sflags.size(), &sflags_d);
   if (!rc) rc = p->mem.upload(work_ord.data(), work_ord.size(), &work_ord_d);
+  if (!rc) rc = p->mem.upload(work_mul.data(), work_mul.size(), &work_mul_d);
   if (!rc) rc = p->mem.upload(iso.data(), iso.size(), &iso_d);
   if (!rc) rc = p->mem.upload(bnd.data(), bnd.size(), &bnd_d);
   const size_t sn = static_cast<size_t>(desc->side_nodes);
@@ -812,6 +820,7 @@ int tdg_plan_create(const tdg_plan_desc* desc, tdg_plan** out) {
   d.work_aff = work_aff_d;
   d.side_flags = sflags_d;
   d.work_ord = work_ord_d;
+  d.work_mul = work_mul_d;
   d.nside_iso = static_cast<int>(iso.size());
   d.side_iso = iso_d;
   d.nside_bnd = static_cast<int>(bnd.size());

@@ -64,6 +64,9 @@ struct DevPlan {
   const int2* work;
   const int* work_aff;   // per work item: 1 if every element of the item is affine
   const int* work_ord;   // per work item: its (N1, N2, N3), read without waiting for work[]
+  // per work item: multipliers m(d) = ceil(2^20 / d) for d = n, n1p, n2p,
+  // n1p n2p and the face nodes per element, [8] per item (mdiv below)
+  const int* work_mul;
   int nsm;        // SMs: kernels prefetch the work about one wave ahead (L2)
   int pf_trace, pf_face, pf_down;   // look-ahead distances, blocks per SM
   int pf_item;    // element kernels: L2 bulk prefetch of the item's own spans
@@ -228,6 +231,48 @@ __device__ __forceinline__ void l2_prefetch_span(const void* p, size_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<unsigned>(e - a))
                : "memory");
 }
+
+// x / d for 0 <= x <= 2048 and 1 <= d <= 512 as a multiply and a shift with
+// m = ceil(2^20 / d) (exact: x (m d - 2^20) < 2^20).  A division by a runtime
+// divisor costs ~20 instructions, three of them on the conversion pipe; the
+// runtime-order kernels decompose node and face indices several times per node.
+constexpr int MDIV_SHIFT = 20;
+__host__ __device__ __forceinline__ int mdiv_mul(int d) { return ((1 << MDIV_SHIFT) + d - 1) / d; }
+__device__ __forceinline__ int mdiv(int x, int m) {
+  return static_cast<int>((static_cast<unsigned>(x) * static_cast<unsigned>(m)) >> MDIV_SHIFT);
+}
+// per-item divisors of the element kernels: compile-time orders divide by
+// constants, runtime orders use the plan's multipliers
+template <int NX>
+struct ItemDiv {
+  int n, n1p, n2p, n12, per_e;
+  int mn, m1, m2, m12, mpe;
+  __device__ __forceinline__ ItemDiv(const int* mul, int n_, int n1p_, int n2p_, int n3p_)
+      : n(n_), n1p(n1p_), n2p(n2p_), n12(n1p_ * n2p_),
+        per_e(2 * (n2p_ * n3p_ + n1p_ * n3p_ + n1p_ * n2p_)) {
+    if (NX < 0) {
+      mn = mul[0];
+      m1 = mul[1];
+      m2 = mul[2];
+      m12 = mul[3];
+      mpe = mul[4];
+    } else {
+      mn = m1 = m2 = m12 = mpe = 0;
+    }
+  }
+  __device__ __forceinline__ int by_n(int x) const { return NX < 0 ? mdiv(x, mn) : x / n; }
+  __device__ __forceinline__ int by_n1p(int x) const { return NX < 0 ? mdiv(x, m1) : x / n1p; }
+  __device__ __forceinline__ int by_n2p(int x) const { return NX < 0 ? mdiv(x, m2) : x / n2p; }
+  __device__ __forceinline__ int by_n12(int x) const { return NX < 0 ? mdiv(x, m12) : x / n12; }
+  __device__ __forceinline__ int by_per_e(int x) const { return NX < 0 ? mdiv(x, mpe) : x / per_e; }
+  // node -> (i, j, k)
+  __device__ __forceinline__ void ijk(int node, int& i, int& j, int& k) const {
+    k = by_n12(node);
+    const int r = node - k * n12;
+    j = by_n1p(r);
+    i = r - j * n1p;
+  }
+};
 
 // a[i] for i in 0..2 as selects (a runtime index into a local array would
 // put the array in local memory)

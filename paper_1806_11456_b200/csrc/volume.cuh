@@ -428,14 +428,14 @@ __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T,
 
 // This thread's NPT nodes' state, loaded before the block's table barrier so
 // that the loads are in flight while the spectral tables are staged.
-template <int NV>
+template <int NV, class Div>
 __device__ __forceinline__ void load_item_state(const DevPlan& P, const double* __restrict__ Q, int2 wi,
-                                                int n, int tot, double (&q)[NPT][NV]) {
+                                                int n, int tot, double (&q)[NPT][NV], const Div& dv) {
 #pragma unroll
   for (int r = 0; r < NPT; ++r) {
     const int t = threadIdx.x + r * blockDim.x;
     if (t < tot) {
-      const int e = t / n, node = t - e * n;
+      const int e = dv.by_n(t), node = t - e * n;
       const long long base = P.node_off[wi.x + e] * NV;
 #pragma unroll
       for (int v = 0; v < NV; ++v) q[r][v] = Q[base + (long long)v * n + node];
@@ -445,10 +445,10 @@ __device__ __forceinline__ void load_item_state(const DevPlan& P, const double* 
 
 // Stage g(q) (and, on curved items, the 9 metric terms Ja) for the thread's
 // nodes in shared memory.
-template <int LAW>
+template <int LAW, class Div>
 __device__ __forceinline__ void stage_grad_vars(const DevPlan& P, int2 wi, int n, int tot, bool aff,
                                                 const double (&q)[NPT][Law<LAW>::NV], double* gs,
-                                                double* js) {
+                                                double* js, const Div& dv) {
   using L = Law<LAW>;
   constexpr int NGV = L::NGV;
 #pragma unroll
@@ -460,7 +460,7 @@ __device__ __forceinline__ void stage_grad_vars(const DevPlan& P, int2 wi, int n
 #pragma unroll
       for (int k = 0; k < NGV; ++k) gs[k * tot + t] = g[k];
       if (!aff) {
-        const int e = t / n, node = t - e * n;
+        const int e = dv.by_n(t), node = t - e * n;
         int ms;
         const double* m = metric_ptr(P, wi.x + e, node, n, ms);
 #pragma unroll
@@ -473,10 +473,9 @@ __device__ __forceinline__ void stage_grad_vars(const DevPlan& P, int2 wi, int n
 // Side and face node of the item-local face task u (u < E * per_e): tasks run
 // element by element, side by side (0..5), face node by face node — the order
 // of P.side_off, so u is also the node offset into the item's side arrays.
-__device__ __forceinline__ void face_task(int u, int per_e, int nf0, int nf1, int nf2, int& e, int& s,
+__device__ __forceinline__ void face_task(int u, int e, int per_e, int nf0, int nf1, int nf2, int& s,
                                           int& kf, int& nf) {
-  e = u / per_e;
-  int r = u - e * per_e;
+  int r = u - e * per_e;   // e = u / per_e, formed by the caller (ItemDiv)
   if (r < 2 * nf0) {
     s = r >= nf0;
     kf = r - s * nf0;
@@ -514,10 +513,11 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift(DevPlan P,
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
+  const ItemDiv<NX> dv(P.work_mul + 8 * blockIdx.x, n, n1p, n2p, n3p);
   double qa[NPT][NV];
   PHASE_DECL;
   PHASE_T(0);
-  load_item_state<NV>(P, Q, wi, n, tot, qa);
+  load_item_state<NV>(P, Q, wi, n, tot, qa, dv);
   prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
   if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
   load_tables(P, N1, N2, N3, T);
@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift(DevPlan P,
   double* gs = sm;               // [NGV][tot]
   double* js = sm + NGV * tot;   // [9][tot]  (curved items only)
   // staging needs no table: one barrier covers both
-  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
+  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js, dv);
   PHASE_T(1);
   __syncthreads();
   PHASE_T(2);
@@ -533,8 +533,9 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift(DevPlan P,
   // when the lift runs), so no value is held across a barrier
 #pragma unroll 1
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
-    const int e = t / n, node = t - e * n, slot = wi.x + e;
-    const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+    const int e = dv.by_n(t), node = t - e * n, slot = wi.x + e;
+    int i, j, k;
+    dv.ijk(node, i, j, k);
     double x[NG];
     lift_node<LAW, NX>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
     const long long gb = P.node_off[slot] * NG;
@@ -564,14 +565,15 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift(DevPlan P,
     double* fvs = sm + NGV * tot;   // [NTR][nfi]
     const long long so0 = P.side_off[wi.x * 6];
     for (int u = threadIdx.x; u < nfi; u += blockDim.x) {
-      int e, s, kf, nf;
-      face_task(u, per_e, nf0, nf1, nf2, e, s, kf, nf);
+      int s, kf, nf;
+      const int e = dv.by_per_e(u);
+      face_task(u, e, per_e, nf0, nf1, nf2, s, kf, nf);
       const int slot = wi.x + e;
       int d, a, b;
       side_dirs(s, d, a, b);
       const int na = sel3(a, n1p, n2p, n3p), nd = sel3(d, n1p, n2p, n3p);
       const int sd = sel3(d, strides[0], strides[1], strides[2]);
-      const int ib = kf / na, ia = kf - ib * na;
+      const int ib = d == 0 ? dv.by_n2p(kf) : dv.by_n1p(kf), ia = kf - ib * na;
       const int off0 = ia * sel3(a, strides[0], strides[1], strides[2]) +
                        ib * sel3(b, strides[0], strides[1], strides[2]);
       const int fl = P.side_flags[slot * 6 + s];
@@ -668,6 +670,7 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own(DevPla
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
+  const ItemDiv<NX> dv(P.work_mul + 8 * blockIdx.x, n, n1p, n2p, n3p);
   const int nf0 = n2p * n3p, nf1 = n1p * n3p, nf2 = n1p * n2p;
   const int per_e = 2 * (nf0 + nf1 + nf2), nfi = wi.y * per_e;
   const bool gst = coupled && P.gstar;
@@ -696,15 +699,16 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own(DevPla
       bulk_g2s(qs, reinterpret_cast<const void*>(lo), static_cast<uint32_t>(hi - lo), &qbar);
     }
   } else {
-    load_item_state<NV>(P, Q, wi, n, tot, qa);
+    load_item_state<NV>(P, Q, wi, n, tot, qa, dv);
     if (P.pf_item) prefetch_item_metrics(P, wi, n, 32);
   }
   if (!gst) prefetch_item_surface<NG>(P, P.lsurf, wi, N1, N2);
   if (gst) {
     // pass 1: g* and n sigma of the conforming interior sides
     for (int u = threadIdx.x; u < nfi; u += blockDim.x) {
-      int e, s, kf, nf;
-      face_task(u, per_e, nf0, nf1, nf2, e, s, kf, nf);
+      int s, kf, nf;
+      const int e = dv.by_per_e(u);
+      face_task(u, e, per_e, nf0, nf1, nf2, s, kf, nf);
       const int4 sn = P.side_nb[(wi.x + e) * 6 + s];
       if (kf == 0) side_on[e * 6 + s] = sn.x >= 0;
       if (sn.x < 0) continue;
@@ -739,7 +743,7 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own(DevPla
     for (int r = 0; r < NPT; ++r) {
       const int t = threadIdx.x + r * blockDim.x;
       if (t < tot) {
-        const int e = t / n, node = t - e * n;
+        const int e = dv.by_n(t), node = t - e * n;
 #pragma unroll
         for (int v = 0; v < NV; ++v) qa[r][v] = qs[shift + (e * NV + v) * n + node];
       }
@@ -747,14 +751,15 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own(DevPla
   }
   const bool aff = P.work_aff[blockIdx.x] != 0;
   // staging needs no table: one barrier covers both
-  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
+  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js, dv);
   __syncthreads();
   const SurfStage SS{sf, side_on, nfi, per_e};
   // pass 2
 #pragma unroll 1
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
-    const int e = t / n, node = t - e * n, slot = wi.x + e;
-    const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+    const int e = dv.by_n(t), node = t - e * n, slot = wi.x + e;
+    int i, j, k;
+    dv.ijk(node, i, j, k);
     double x[NG];
     if (gst)
       lift_node<LAW, NX, 1>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x, SS);
@@ -788,13 +793,14 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own(DevPla
     __syncthreads();   // the block's gradient stores are visible to the block
     const long long so0 = P.side_off[wi.x * 6];
     for (int u = threadIdx.x; u < nfi; u += blockDim.x) {
-      int e, s, kf, nf;
-      face_task(u, per_e, nf0, nf1, nf2, e, s, kf, nf);
+      int s, kf, nf;
+      const int e = dv.by_per_e(u);
+      face_task(u, e, per_e, nf0, nf1, nf2, s, kf, nf);
       const int slot = wi.x + e;
       int d, a, b;
       side_dirs(s, d, a, b);
       const int na = sel3(a, n1p, n2p, n3p), nd = sel3(d, n1p, n2p, n3p);
-      const int ib = kf / na, ia = kf - ib * na;
+      const int ib = d == 0 ? dv.by_n2p(kf) : dv.by_n1p(kf), ia = kf - ib * na;
       const int off = ia * sel3(a, 1, n1p, n1p * n2p) + ib * sel3(b, 1, n1p, n1p * n2p) +
                       ((s & 1) ? (nd - 1) * sel3(d, 1, n1p, n1p * n2p) : 0);
       const long long so = so0 + u - kf;
@@ -834,6 +840,7 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own_inl(De
   const int N1 = NX >= 0 ? NX : od[0], N2 = NX >= 0 ? NX : od[1], N3 = NX >= 0 ? NX : od[2];
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
+  const ItemDiv<NX> dv(P.work_mul + 8 * blockIdx.x, n, n1p, n2p, n3p);
   double qa[NPT][NV];
   __shared__ unsigned long long qbar;
   double* gs = sm;               // [NGV][tot]
@@ -866,13 +873,13 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own_inl(De
     for (int r = 0; r < NPT; ++r) {
       const int t = threadIdx.x + r * blockDim.x;
       if (t < tot) {
-        const int e = t / n, node = t - e * n;
+        const int e = dv.by_n(t), node = t - e * n;
 #pragma unroll
         for (int v = 0; v < NV; ++v) qa[r][v] = qs[shift + (e * NV + v) * n + node];
       }
     }
   } else {
-    load_item_state<NV>(P, Q, wi, n, tot, qa);
+    load_item_state<NV>(P, Q, wi, n, tot, qa, dv);
     if (coupled && P.gstar)
       prefetch_item_gstar<NGV>(P, wi, N1, N2, N3);
     else
@@ -882,12 +889,13 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_lift_own_inl(De
   }
   const bool aff = P.work_aff[blockIdx.x] != 0;
   // staging needs no table: one barrier covers both
-  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js);
+  stage_grad_vars<LAW>(P, wi, n, tot, aff, qa, gs, js, dv);
   __syncthreads();
 #pragma unroll 1
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
-    const int e = t / n, node = t - e * n, slot = wi.x + e;
-    const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+    const int e = dv.by_n(t), node = t - e * n, slot = wi.x + e;
+    int i, j, k;
+    dv.ijk(node, i, j, k);
     double x[NG];
     if (coupled && P.gstar)
       lift_node<LAW, NX, 2>(P, T, gs, js, aff, tot, n, n1p, n2p, n3p, e, node, slot, i, j, k, x);
@@ -972,6 +980,7 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_flux(DevPlan P,
   }
   const int n1p = N1 + 1, n2p = N2 + 1, n3p = N3 + 1;
   const int n = n1p * n2p * n3p, tot = wi.y * n;
+  const ItemDiv<NX> dv(P.work_mul + 8 * blockIdx.x, n, n1p, n2p, n3p);
   double* ft = sm;   // [3][NV][tot]
   const bool visc = L::viscous(P.prm);
   PHASE_DECL;
@@ -982,7 +991,7 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_flux(DevPlan P,
   for (int r = 0; r < NPT; ++r) {
     const int t = threadIdx.x + r * blockDim.x;
     if (t < tot) {
-      const int e = t / n, node = t - e * n, slot = wi.x + e;
+      const int e = dv.by_n(t), node = t - e * n, slot = wi.x + e;
       const long long base = P.node_off[slot] * NV;
       double q[NV], f[3][NV];
 #pragma unroll
@@ -1017,8 +1026,9 @@ __global__ void __launch_bounds__(VOL_THREADS, VOL_BLOCKS) k_vol_flux(DevPlan P,
   for (int r = 0; r < NPT; ++r) {
     const int t = threadIdx.x + r * blockDim.x;
     if (t < tot) {
-      const int e = t / n, node = t - e * n, slot = wi.x + e;
-      const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+      const int e = dv.by_n(t), node = t - e * n, slot = wi.x + e;
+      int i, j, k;
+    dv.ijk(node, i, j, k);
       const int eb = e * n;
       double F[NV], F0[NV], F1[NV], F2[NV];   // per-direction chains (ILP)
 #pragma unroll
@@ -1177,10 +1187,11 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_element_dt(DevPlan P, const do
   const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int No[3] = {od[0], od[1], od[2]};
   const int n = (No[0] + 1) * (No[1] + 1) * (No[2] + 1), tot = wi.y * n;
+  const ItemDiv<-1> dv(P.work_mul + 8 * blockIdx.x, n, No[0] + 1, No[1] + 1, No[2] + 1);
   for (int u = threadIdx.x; u < MAX_ITEM_ELEMS; u += blockDim.x) smax[u] = 0ull;
   __syncthreads();
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
-    const int e = t / n, node = t - e * n, slot = wi.x + e;
+    const int e = dv.by_n(t), node = t - e * n, slot = wi.x + e;
     const long long base = P.node_off[slot] * NV;
     double q[NV];
 #pragma unroll
@@ -1220,12 +1231,13 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_norm(DevPlan P, const double* 
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int n = (od[0] + 1) * (od[1] + 1) * (od[2] + 1), tot = wi.y * n;
+  const ItemDiv<-1> dv(P.work_mul + 8 * blockIdx.x, n, od[0] + 1, od[1] + 1, od[2] + 1);
   for (int u = threadIdx.x; u < MAX_ITEM_ELEMS; u += blockDim.x) emax[u] = 0ull;
   __syncthreads();
   double m = 0.0;
   bool bad = false;
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
-    const int e = t / n, node = t - e * n, slot = wi.x + e;
+    const int e = dv.by_n(t), node = t - e * n, slot = wi.x + e;
     const long long base = P.node_off[slot] * NV + node;
     double em = 0.0;
 #pragma unroll
@@ -1257,13 +1269,15 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_tau_avalue(DevPlan P, const do
   const int2 wi = P.work[blockIdx.x];
   const int* od = P.work_ord + 3 * blockIdx.x;
   const int n1p = od[0] + 1, n2p = od[1] + 1, n = n1p * n2p * (od[2] + 1), tot = wi.y * n;
+  const ItemDiv<-1> dv(P.work_mul + 8 * blockIdx.x, n, n1p, n2p, od[2] + 1);
   for (int u = threadIdx.x; u < MAX_ITEM_ELEMS; u += blockDim.x) emax[u] = 0ull;
   for (int u = threadIdx.x; u < 24; u += blockDim.x)
     w[u / 8][u % 8] = P.tables[OFF_W + sel3(u / 8, od[0], od[1], od[2]) * 8 + (u % 8)];
   __syncthreads();
   for (int t = threadIdx.x; t < tot; t += blockDim.x) {
-    const int e = t / n, node = t - e * n, slot = wi.x + e;
-    const int i = node % n1p, j = (node / n1p) % n2p, k = node / (n1p * n2p);
+    const int e = dv.by_n(t), node = t - e * n, slot = wi.x + e;
+    int i, j, k;
+    dv.ijk(node, i, j, k);
     int ms;
     const double* mp = metric_ptr(P, slot, node, n, ms);
     const double mass = w[0][i] * w[1][j] * w[2][k] * mp[0];
