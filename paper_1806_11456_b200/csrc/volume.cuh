@@ -409,9 +409,11 @@ __device__ __forceinline__ void lift_node(const DevPlan& P, const ElemTables& T,
 #pragma unroll
         for (int d2 = 0; d2 < 3; ++d2) ns[d2] = sp[(NGV + d2) * SS.nfi];
 #pragma unroll
+        for (int kk = 0; kk < NGV; ++kk) g[kk] *= lw;
+#pragma unroll
         for (int d2 = 0; d2 < 3; ++d2)
 #pragma unroll
-          for (int kk = 0; kk < NGV; ++kk) acc[d2 * NGV + kk] += lw * (g[kk] * ns[d2]);
+          for (int kk = 0; kk < NGV; ++kk) acc[d2 * NGV + kk] += g[kk] * ns[d2];
         continue;
       }
     }
