@@ -3,6 +3,7 @@
 # Everything lands in gpurun_out/ev/; copy the summaries into profiles/rNN/.
 set -x
 mkdir -p gpurun_out/ev /tmp/rep
+rm -f /tmp/rep/*.ncu-rep   # a reused box keeps /tmp: never read a stale report
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > gpurun_out/ev/smi.txt
 export PARITY_REPORT=$PWD/gpurun_out/ev/parity.jsonl
 rm -f $PARITY_REPORT
@@ -18,10 +19,10 @@ timeout 600 python bench.py --quick --steps 2 --warmup 3 --no-cpu-baseline --vcy
     > gpurun_out/ev/ncu_ll.log 2>&1
 # full-set captures of one config-3 and one config-4 residual
 python tools/prof_residual.py --config 3 --n 32 --evals 1 > gpurun_out/ev/p3.txt 2>&1 && \
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_vol_|k_mortar|k_trace|k_face" -c 7 \
+  timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:"k_vol_|k_mortar|k_trace|k_face" -c 7 \
     -o /tmp/rep/cfg3 python tools/prof_residual.py --config 3 --n 32 --evals 1 > gpurun_out/ev/ncu3.log 2>&1
 python tools/prof_residual.py --config 4 --n 24 --evals 1 > gpurun_out/ev/p4.txt 2>&1 && \
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_vol_|k_trace|k_face" -c 5 \
+  timeout 600 ncu -f --set full --clock-control none --import-source on -k regex:"k_vol_|k_trace|k_face" -c 5 \
     -o /tmp/rep/cfg4 python tools/prof_residual.py --config 4 --n 24 --evals 1 > gpurun_out/ev/ncu4.log 2>&1
 for c in cfg3 cfg4; do
   ncu -i /tmp/rep/$c.ncu-rep --page raw --csv > gpurun_out/ev/${c}_raw.csv 2>/dev/null
