@@ -291,7 +291,10 @@ int run_surface(tdg_plan* p, const DevPlan& d, const double* Q, int isolated, cu
   const int coupled = isolated ? 0 : 1;
   if (!traces_fresh) {
     KTimer kt(TDG_K_TRACE, st);
-    k_trace_q<L::NV><<<d.nwork, p->trace_threads, 0, st>>>(d, Q, coupled);
+    // mortar plans, coupled evaluation: the item's Q span is staged in shared memory
+    const size_t smem_trace = (coupled && d.nmface != 0)
+                                  ? (static_cast<size_t>(L::NV) * p->max_tot + 2) * sizeof(double) : 0;
+    k_trace_q<L::NV><<<d.nwork, p->trace_threads, smem_trace, st>>>(d, Q, coupled);
     LAUNCH_CHECK("k_trace_q");
   }
   p->traces_of = Q;

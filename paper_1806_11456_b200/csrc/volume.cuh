@@ -185,6 +185,8 @@ template <int NV>
 __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const double* __restrict__ Q,
                                                           int coupled) {
   __shared__ double sb[3][16];
+  __shared__ unsigned long long qbar;
+  extern __shared__ double qsm[];   // mortar plans: the item's Q span ([nv][n] x E)
   const int2 wi = P.work[blockIdx.x];
   {
     const int2 wn = item_ahead(P, P.pf_trace);
@@ -192,11 +194,29 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
   }
   const int* od = P.work_ord + 3 * blockIdx.x;   // item orders: no hop through wi
   const int No[3] = {od[0], od[1], od[2]};
-  for (int u = threadIdx.x; u < 48; u += blockDim.x)
-    sb[u / 16][u % 16] = P.tables[OFF_BND + sel3(u / 16, No[0], No[1], No[2]) * 16 + (u % 16)];
-  __syncthreads();
   const int np[3] = {No[0] + 1, No[1] + 1, No[2] + 1};
   const int n = np[0] * np[1] * np[2];
+  // Mortar plans: the warp-per-side pass reads its face layers as strided
+  // gathers (8.5 sectors moved per sector used when read from global memory);
+  // the item's slots are contiguous in Q, so one TMA bulk copy stages them in
+  // shared memory instead (16-byte aligned span, data `shift` doubles in).
+  const bool staged = coupled && P.nmface != 0;
+  int shift = 0;
+  if (staged) {
+    const double* src = Q + P.node_off[wi.x] * NV;
+    shift = static_cast<int>((reinterpret_cast<unsigned long long>(src) & 15ull) >> 3);
+    if (threadIdx.x == 0) {
+      mbar_init(&qbar, 1);
+      mbar_fence_init();
+      const unsigned long long a = reinterpret_cast<unsigned long long>(src);
+      const unsigned long long lo = a & ~15ull, hi = (a + 8ull * NV * n * wi.y + 15ull) & ~15ull;
+      mbar_expect_tx(&qbar, static_cast<uint32_t>(hi - lo));
+      bulk_g2s(qsm, reinterpret_cast<const void*>(lo), static_cast<uint32_t>(hi - lo), &qbar);
+    }
+  }
+  for (int u = threadIdx.x; u < 48; u += blockDim.x)
+    sb[u / 16][u % 16] = P.tables[OFF_BND + sel3(u / 16, No[0], No[1], No[2]) * 16 + (u % 16)];
+  __syncthreads();   // tables staged; mbarrier initialised before anyone waits on it
   const int strides[3] = {1, np[0], np[0] * np[1]};
   if (!coupled || P.nmface == 0) {
     // every side on own-order traces: (element, side, face node) flattened
@@ -236,10 +256,9 @@ __global__ void __launch_bounds__(ELEM_THREADS) k_trace_q(DevPlan P, const doubl
     }
     return;
   }
+  mbar_wait(&qbar, 0);
   item_side_traces<NV>(P, wi.x, wi.y, coupled, np, strides, sb, P.qtr, P.qtrm,
-                           [&](int e, int c, int off) {
-                             return Q[(P.node_off[wi.x + e] * NV) + (long long)c * n + off];
-                           });
+                       [&](int e, int c, int off) { return qsm[shift + (e * NV + c) * n + off]; });
 }
 
 // Branch-free surface gather for LGL items with at least two nodes per
