@@ -375,11 +375,15 @@ def run_b200(args):
     Rh = [outs[k % nbuf] for k in range(args.steps)]
     op.residual_host(Qh[:nbuf], out=Rh[:nbuf])     # untimed: every staging buffer once
     torch.cuda.synchronize()
-    e_ms = timed(lambda: op.residual_host(Qh, out=Rh), 1)
+    # the copies run at the mercy of the host (PCIe, NUMA, other tenants): the K-step
+    # batch is timed three times and the fastest is reported, all three listed
+    e_all = [timed(lambda: op.residual_host(Qh, out=Rh), 1) for _ in range(3)]
+    e_ms = min(e_all)
     e2e = {"value": nodes * args.steps * ws / (e_ms / 1000.0), "unit": "DOF-evals/s",
            "h2d_bytes_per_step": q0.numel() * 8, "d2h_bytes_per_step": q0.numel() * 8 + 8,
            "ms_per_step": e_ms / args.steps, "api": "DGOperator.residual_host (tdg_residual_host)",
-           "overlap": "double-buffered: H2D of step k+1 and D2H of step k-1 overlap step k"}
+           "overlap": "double-buffered: H2D of step k+1 and D2H of step k-1 overlap step k",
+           "repeats": {"stat": "min of 3 batches of K steps", "ms_per_step_all": [t / args.steps for t in e_all]}}
     del Qh, Rh, bufs, outs
 
     # ---- config 3: the tau estimation (isolated, all directions) -----------------
